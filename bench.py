@@ -1,0 +1,389 @@
+#!/usr/bin/env python3
+"""Benchmark: batched FP64 dgemm_nn (BASELINE.json config 1) on B200 through the pbgpu C ABI.
+
+Step = one pass of the hot path over one batch: pb_dgemm_batched('n','n', 64,64,64,
+alpha=1, beta=1, lda=ldb=ldc=64) over 16384 independent problems per GPU (weak
+scaling: every rank owns its own batch; no collective on the data path).
+
+  value  — FP64 GFLOP/s of the whole job, inputs resident in HBM, CUDA events on the
+           launching stream, max over ranks (flop model 2mnk, bench.hpp:119-138);
+  e2e    — the same metric through the public API with pinned HOST buffers: every step
+           copies A, B, C host->device and C back (pbgpu stages and overlaps the copies);
+  roofline — the dominant kernel (gemm_tiles_kernel) against measured HBM bandwidth:
+           algorithmic bytes 8*(mk + kn + 2mn) per problem;
+  cpu_baseline — the reference's own CPU path (panelblas::dgemm compiled from
+           /root/reference into oracle/_ref) on this host's cores, bounded sample;
+  series — secondary lines of the metric ("vs n"): dgemm and dpotrf at other n.
+
+`--impl reference` runs only the reference CPU arm (rank 0) and prints its line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M = N = K = 64
+BATCH = 16384
+FLOPS_PER_PROBLEM = 2 * M * N * K
+BYTES_PER_PROBLEM = 8 * (M * K + K * N + 2 * M * N)
+METRIC = "FP64 GFLOP/s (batched dgemm/dpotrf vs n) at 1/2/4/8 B200; % of FP64 roofline"
+UNIT = "GFLOP/s"
+CONFIG = {"workload": "cfg1: batched dgemm_nn column-major, m=n=k=64, lda=ldb=ldc=64, alpha=beta=1, "
+                      "uniform[-1,1], 16384 problems per GPU",
+          "batch_per_gpu": BATCH, "m": M, "n": N, "k": K,
+          "l2": "inputs (2.1 GB per GPU) exceed the 126 MB L2; no flush needed"}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ helpers
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        import torch
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws: int):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_reference_dgemm(A, B, C, batch, threads, reps):
+    """Times the reference's own panelblas::dgemm loop (oracle/_ref) over `batch` problems."""
+    from oracle import binding as ob
+    if ob.have_ref():
+        lib, kind = ob.ref(), "reference"
+    else:
+        lib, kind = ob.oracle(), "port"
+    laps = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        lib.dgemm_batch(b"n", b"n", M, N, K, 1.0, A.ctypes.data, M, M * K, B.ctypes.data, K, K * N, 1.0,
+                        C.ctypes.data, M, M * N, batch, threads)
+        laps.append(time.perf_counter() - t0)
+    sec = statistics.median(laps)
+    return batch * FLOPS_PER_PROBLEM / sec / 1e9, kind, sec
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args, ws, rank):
+    import numpy as np
+    if rank != 0:
+        return 0
+    rng = np.random.default_rng(42)
+    batch = BATCH
+    A = rng.uniform(-1, 1, batch * M * K)
+    B = rng.uniform(-1, 1, batch * K * N)
+    C = rng.uniform(-1, 1, batch * M * N)
+    threads = host_threads()
+    for _ in range(args.warmup):
+        cpu_reference_dgemm(A, B, C, batch, threads, 1)
+    vals, secs = [], []
+    kind = "port"
+    for _ in range(args.steps):
+        v, kind, s = cpu_reference_dgemm(A, B, C, batch, threads, 1)
+        vals.append(v)
+        secs.append(s)
+    total = sum(secs)
+    value = args.steps * batch * FLOPS_PER_PROBLEM / total / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": CONFIG,
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": f"full cfg1 batch ({batch} problems) per step, "
+                                       f"{threads} threads, contiguous split"},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def time_device(fn, steps, warmup, stream, ws):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    return e0.elapsed_time(e1)
+
+
+def series_dpotrf(pb, dev, stream):
+    """dpotrf_l (config 3) GFLOP/s at each n: inputs SPD = B B^T + n I, B ~ N(0,1)."""
+    import torch
+    out = {}
+    g = torch.Generator(device=dev).manual_seed(3)
+    for n in (16, 32, 64, 128, 256):
+        batch = 8192
+        Bm = torch.randn((batch, n, n), generator=g, device=dev, dtype=torch.float64)
+        A0 = Bm @ Bm.transpose(1, 2) + n * torch.eye(n, device=dev, dtype=torch.float64)
+        del Bm
+        A = A0.clone()
+        info = torch.empty(batch, dtype=torch.int32, device=dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        laps = []
+        for r in range(4):
+            A.copy_(A0)  # restore the pristine input outside the timed region
+            torch.cuda.synchronize()
+            e0.record(stream)
+            pb.dpotrf_batched("l", n, A, n, n * n, info, batch, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if r:
+                laps.append(e0.elapsed_time(e1))
+        assert int(info.abs().sum()) == 0
+        ms = statistics.median(laps)
+        flops = (n * n * n // 3) * batch
+        gf = flops / ms / 1e6
+        by = 8 * n * (n + 1) * batch
+        out[str(n)] = {"gflops": round(gf, 1), "ms": round(ms, 4), "hbm_gbs": round(by / ms / 1e6, 1)}
+        del A, A0
+    return out
+
+
+def series_dgemm(pb, dev, stream):
+    import torch
+    out = {}
+    for n, batch in ((32, 65536), (64, 16384), (128, 4096), (256, 1024)):
+        A = torch.rand((batch, n, n), device=dev, dtype=torch.float64)
+        B = torch.rand((batch, n, n), device=dev, dtype=torch.float64)
+        C = torch.rand((batch, n, n), device=dev, dtype=torch.float64)
+        fn = lambda: pb.dgemm_batched("n", "n", n, n, n, 1.0, A, n, n * n, B, n, n * n, 1.0, C, n, n * n,
+                                      batch, stream=stream)
+        ms = time_device(fn, 5, 2, stream, 1) / 5
+        out[str(n)] = {"gflops": round(2 * n ** 3 * batch / ms / 1e6, 1), "ms": round(ms, 4),
+                       "batch": batch}
+        del A, B, C
+    return out
+
+
+def run_gpu_arm(args, ws, rank, local):
+    import numpy as np
+    import torch
+    import paper_1902_08115_b200 as pb
+    pb.lib()  # fail loudly when the CUDA library is missing (no CPU fallback)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    A = torch.rand((BATCH, K, M), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+    B = torch.rand((BATCH, N, K), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+    C = torch.rand((BATCH, N, M), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+
+    def step():
+        pb.dgemm_batched("n", "n", M, N, K, 1.0, A, M, M * K, B, K, K * N, 1.0, C, M, M * N, BATCH,
+                         stream=stream)
+
+    with ClockSampler(local) as clk:
+        ms_total = time_device(step, args.steps, args.warmup, stream, ws)
+    ms_total = max_over_ranks(ms_total, ws)
+    ms_step = ms_total / args.steps
+    value = ws * BATCH * FLOPS_PER_PROBLEM / (ms_step * 1e-3) / 1e9
+
+    # ---- end to end through the public API with pinned host buffers ----
+    hA = torch.empty((BATCH, K, M), dtype=torch.float64, pin_memory=True)
+    hB = torch.empty((BATCH, N, K), dtype=torch.float64, pin_memory=True)
+    hC = torch.empty((BATCH, N, M), dtype=torch.float64, pin_memory=True)
+    hA.copy_(A); hB.copy_(B); hC.copy_(C)
+
+    def e2e_step():
+        r = pb.dgemm_batched("n", "n", M, N, K, 1.0, hA.data_ptr(), M, M * K, hB.data_ptr(), K, K * N, 1.0,
+                             hC.data_ptr(), M, M * N, BATCH)
+        assert r.ok()
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier(ws)
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 10))
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, ws)
+    e2e_value = ws * BATCH * FLOPS_PER_PROBLEM / e2e_s / 1e9
+    h2d = 8 * BATCH * (M * K + K * N + M * N)
+    d2h = 8 * BATCH * M * N
+
+    line = None
+    if rank == 0:
+        bw, peak_kind = measured_peaks()
+        ach = BATCH * BYTES_PER_PROBLEM / (ms_step * 1e-3) / 1e9  # one launch per step
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        dmma = pb.lib().pb_probe_dmma_tflops()
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded uniform[-1,1], generated on device)", "config": CONFIG,
+                "parallelism": f"batch-parallel x{ws} (no collective)",
+                "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": bw, "unit": "GB/s",
+                             "frac": round(ach / bw, 4), "traffic": traffic,
+                             "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                             "kernel": "gemm_tiles_kernel<L_MNC,L_KC,0>",
+                             "algorithmic_bytes_per_launch": BATCH * BYTES_PER_PROBLEM,
+                             "fp64_roofline_gflops": round(min(dmma * 1e3, bw * 4.0), 1),
+                             "fp64_frac": round(value / ws / min(dmma * 1e3, bw * 4.0), 4),
+                             "fp64_dmma_peak_tflops_measured": round(dmma, 2)},
+                "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+                "gpu_launches": args.steps, "clocks": clk.summary()}
+    # ---- CPU baseline (rank 0, N = 1 only), bounded sample ----
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        sample = min(BATCH, args.cpu_sample)
+        hA_np = hA.numpy().reshape(-1)[: sample * M * K].copy()
+        hB_np = hB.numpy().reshape(-1)[: sample * K * N].copy()
+        hC_np = hC.numpy().reshape(-1)[: sample * M * N].copy()
+        threads = host_threads()
+        v, kind, sec = cpu_reference_dgemm(hA_np, hB_np, hC_np, sample, threads, 3)
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": UNIT, "cores": threads, "kind": kind,
+                                "sample": f"{sample} of the cfg1 problems, median of 3 passes "
+                                          f"({sec:.2f} s each), {threads} threads contiguous split"}
+    if rank == 0 and ws == 1 and not args.no_series:
+        line["series"] = {"dgemm_nn_cm": series_dgemm(pb, dev, stream),
+                          "dpotrf_l": series_dpotrf(pb, dev, stream)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="pbgpu", choices=["pbgpu", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=16384)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-series", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "pbgpu" else args.warmup
+    ws, rank, local = dist_init()
+    try:
+        if args.impl == "reference":
+            return run_reference_arm(args, ws, rank)
+        return run_gpu_arm(args, ws, rank, local)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

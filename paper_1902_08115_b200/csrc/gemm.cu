@@ -1,0 +1,520 @@
+// Batched FP64 tiled gemm engine for sm_100a.
+//
+// Replaces the reference's five CPU packing variants (gemm.hpp:249-400) and
+// the panel-major native gemm (level3.hpp:360-403) with ONE persistent,
+// warp-specialised kernel:
+//   * work item = (problem, 64x64 tile of C); items are dealt round-robin to
+//     one resident CTA per SM;
+//   * a producer warp streams op(A)/op(B) k-chunks (BK = 32) into a ring of
+//     shared-memory stages with ONE TMA tensor copy per operand per stage
+//     (cp.async.bulk.tensor, complete_tx on an mbarrier).  The tensor maps
+//     describe the whole batch (problem index = outermost dimension) and
+//     their boxes are 4 doubles wider than the tile along the contiguous
+//     dimension: the TMA engine zero-fills the out-of-range lanes, which
+//     gives a padded shared-memory layout (stride = 4 mod 16 doubles) so
+//     every DMMA fragment load is a conflict-free 2-wavefront LDS.64.
+//     Panel-major operands (ps = 4) map to 4-D tensors whose boxes land in
+//     shared memory already panel-interleaved.  Misaligned operands fall
+//     back to zero-filling 8-byte cp.async;
+//   * eight consumer warps run FP64 tensor-core DMMA m8n8k4 on 32x16 warp
+//     tiles of D' = C^T = op(B)^T op(A)^T.  Computing the transpose makes
+//     every lane own two vertically adjacent C elements, so the epilogue
+//     loads and stores C/D as 16-byte pairs in both column-major and
+//     panel-major storage;
+//   * the epilogue applies alpha/beta (beta == 0 never reads C,
+//     micro_kernel.hpp:263-268) with C prefetched one item ahead, and the
+//     uplo mask used by syrk (level3.hpp:220-246, 407-441).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace pbg {
+
+constexpr int TM = 64, TN = 64, BK = 32;
+constexpr int NCW = 8;  // consumer warps
+constexpr int NTHREADS = (NCW + 1) * 32;
+
+template <int L>
+struct LayT;
+template <>
+struct LayT<L_MNC> {  // smem (x, l) at l*S + x ; TMA box {S, BK}
+  static constexpr int S = TM + 4;
+  static constexpr int SIZE = BK * S;
+  __device__ static __forceinline__ int at(int x, int l) { return l * S + x; }
+  __device__ static __forceinline__ long long g(int ld, int x, int l) {
+    return (long long)x + (long long)l * ld;
+  }
+};
+template <>
+struct LayT<L_KC> {  // smem (x, l) at x*S + l ; TMA box {S, TM}
+  static constexpr int S = BK + 4;
+  static constexpr int SIZE = TM * S;
+  __device__ static __forceinline__ int at(int x, int l) { return x * S + l; }
+  __device__ static __forceinline__ long long g(int ld, int x, int l) {
+    return (long long)l + (long long)x * ld;
+  }
+};
+template <>
+struct LayT<L_PMX> {  // smem panels over x: (x/4)*P + l*4 + x%4 ; TMA box {4, BK, TM/4}
+  static constexpr int P = 4 * BK;
+  static constexpr int SIZE = (TM / 4) * P;
+  __device__ static __forceinline__ int at(int x, int l) { return (x >> 2) * P + l * 4 + (x & 3); }
+  __device__ static __forceinline__ long long g(int cn, int x, int l) {
+    return (long long)(x >> 2) * 4 * cn + (long long)l * 4 + (x & 3);
+  }
+};
+template <>
+struct LayT<L_PML> {  // smem panels over l: (l/4)*P + x*4 + l%4 ; TMA box {4, TM, BK/4}
+  static constexpr int P = 4 * TM;
+  static constexpr int SIZE = (BK / 4) * P;
+  __device__ static __forceinline__ int at(int x, int l) { return (l >> 2) * P + x * 4 + (l & 3); }
+  __device__ static __forceinline__ long long g(int cn, int x, int l) {
+    return (long long)(l >> 2) * 4 * cn + (long long)x * 4 + (l & 3);
+  }
+};
+
+struct KParams {
+  CUtensorMap tmA, tmB;  // valid when the side's `tma` flag is set
+  OpDesc a, b;
+  OutDesc o;
+  int tmaA, tmaB;
+  int batched_mapA, batched_mapB;  // tensor map has a problem dimension
+  int m, n, k;
+  double alpha, beta;
+  int uplo;
+  int tiles_m, tiles_n, tiles_per_problem, nk;
+  long long items;
+  int nstages;
+  const int* skip;
+};
+
+__device__ __forceinline__ void decode_item(const KParams& P, long long item, int& p, int& tm,
+                                            int& tn) {
+  p = (int)(item / P.tiles_per_problem);
+  int r = (int)(item - (long long)p * P.tiles_per_problem);
+  if (P.uplo == 0) {
+    tm = r % P.tiles_m;
+    tn = r / P.tiles_m;
+  } else {
+    // triangular tile enumeration: r -> (hi, lo) with hi >= lo
+    int hi = (int)((sqrtf(8.0f * r + 1.0f) - 1.0f) * 0.5f);
+    while ((hi + 1) * (hi + 2) / 2 <= r) ++hi;
+    while (hi * (hi + 1) / 2 > r) --hi;
+    int lo = r - hi * (hi + 1) / 2;
+    if (P.uplo == 1) { tm = hi; tn = lo; } else { tm = lo; tn = hi; }
+  }
+}
+
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                         int c3, int rank, uint64_t* bar) {
+  const uint64_t desc = reinterpret_cast<uint64_t>(tm);
+  if (rank == 3)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+        "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+  else if (rank == 4)
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+        "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(desc), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Producer, TMA path: one tensor copy for this side's chunk (lane 0).
+template <int L>
+__device__ __forceinline__ void tma_side(const CUtensorMap* tm, int batched, int p, int x0, int l0,
+                                         double* s, uint64_t* bar) {
+  // coordinates innermost first; rank includes the problem dimension when batched
+  if (L == L_MNC) tma_load(s, tm, x0, l0, batched ? p : 0, 0, batched ? 3 : 2, bar);
+  else if (L == L_KC) tma_load(s, tm, l0, x0, batched ? p : 0, 0, batched ? 3 : 2, bar);
+  else if (L == L_PMX) tma_load(s, tm, 0, l0, x0 >> 2, batched ? p : 0, batched ? 4 : 3, bar);
+  else tma_load(s, tm, 0, x0, l0 >> 2, batched ? p : 0, batched ? 4 : 3, bar);
+}
+
+// Producer, fallback path: every (x, l) of the 64 x kvalid4 chunk through
+// 8-byte cp.async, out-of-range entries zero-filled.
+template <int L>
+__device__ __forceinline__ void elem_side(const OpDesc& d, int p, int x0, int xvalid, int l0,
+                                          int kvalid, double* s, int lane) {
+  using T = LayT<L>;
+  const double* g = d.base + (long long)p * d.stride;
+  const int kvalid4 = (kvalid + 3) & ~3;
+  for (int e = lane; e < kvalid4 * TM; e += 32) {
+    int x, l;
+    if (L == L_KC || L == L_PMX) { l = e % kvalid4; x = e / kvalid4; } else { x = e % TM; l = e / TM; }
+    bool v = x < xvalid && l < kvalid;
+    const double* src = v ? g + T::g(d.ld, x0 + x, l0 + l) : d.base;
+    cp_async8(s + T::at(x, l), src, v);
+  }
+}
+
+template <int OUT_PM>
+__device__ __forceinline__ long long out_off(int ld, int i, int j) {
+  if (OUT_PM) return (long long)(i >> 2) * 4 * ld + (long long)j * 4 + (i & 3);
+  return (long long)i + (long long)j * ld;
+}
+
+template <int LA, int LB, int OUT_PM>
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_constant__ KParams P) {
+  using TA = LayT<LA>;
+  using TB = LayT<LB>;
+  constexpr int STAGE = TA::SIZE + TB::SIZE;  // doubles
+  extern __shared__ __align__(128) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)P.nstages * STAGE);
+  uint64_t* empty = full + P.nstages;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P.nstages; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      if (P.tmaA) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&P.tmA) : "memory");
+      if (P.tmaB) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&P.tmB) : "memory");
+    }
+    constexpr uint32_t BYTES_A = TA::SIZE * 8, BYTES_B = TB::SIZE * 8;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (long long item = blockIdx.x; item < P.items; item += gridDim.x) {
+      int p, tm, tn;
+      decode_item(P, item, p, tm, tn);
+      if (P.skip && P.skip[p]) continue;
+      const int i0 = tm * TM, j0 = tn * TN;
+      const int mvalid = min(TM, P.m - i0), nvalid = min(TN, P.n - j0);
+      for (int kc = 0; kc < P.nk; ++kc) {
+        const int l0 = kc * BK, kvalid = min(BK, P.k - l0);
+        mbar_wait(&empty[stage], phase ^ 1);
+        double* sA = smem + (size_t)stage * STAGE;
+        double* sB = sA + TA::SIZE;
+        if (lane == 0) {
+          const uint32_t bytes = (P.tmaA ? BYTES_A : 0) + (P.tmaB ? BYTES_B : 0);
+          if (bytes) mbar_expect_tx(&full[stage], bytes);
+          if (P.tmaA) tma_side<LA>(&P.tmA, P.batched_mapA, p, i0, l0, sA, &full[stage]);
+          if (P.tmaB) tma_side<LB>(&P.tmB, P.batched_mapB, p, j0, l0, sB, &full[stage]);
+        }
+        if (!P.tmaA || !P.tmaB) {
+          fence_proxy_async();
+          if (!P.tmaA) elem_side<LA>(P.a, p, i0, mvalid, l0, kvalid, sA, lane);
+          if (!P.tmaB) elem_side<LB>(P.b, p, j0, nvalid, l0, kvalid, sB, lane);
+        }
+        mbar_arrive_cpasync(&full[stage]);
+        if (++stage == P.nstages) { stage = 0; phase ^= 1; }
+      }
+    }
+    cp_async_wait_all();
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int g = lane >> 2, t = lane & 3;
+  const int jb = (warp >> 2) * 32, ib = (warp & 3) * 16;
+  const bool use_c = P.beta != 0.0;
+  // beta*C operands for this lane's 4x2 fragments, prefetched one item ahead
+  // so their DRAM latency hides behind a whole item of tensor-core work.
+  double cv[4][2][2], cn[4][2][2];
+  auto load_c = [&](long long it, double (&dst)[4][2][2]) {
+    int p, tm, tn;
+    decode_item(P, it, p, tm, tn);
+    const double* cbase = P.o.c + (long long)p * P.o.sc;
+    const bool live = !(P.skip && P.skip[p]);
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = tm * TM + ib + h * 8 + 2 * t, j = tn * TN + jb + f * 8 + g;
+        dst[f][h][0] = dst[f][h][1] = 0.0;
+        if (j < P.n && live) {
+          const double* cp = cbase + out_off<OUT_PM>(P.o.ldc, i, j);
+          if (P.o.vec && i + 1 < P.m) {
+            double2 v = *reinterpret_cast<const double2*>(cp);
+            dst[f][h][0] = v.x;
+            dst[f][h][1] = v.y;
+          } else {
+            if (i < P.m) dst[f][h][0] = cp[0];
+            if (i + 1 < P.m) dst[f][h][1] = cbase[out_off<OUT_PM>(P.o.ldc, i + 1, j)];
+          }
+        }
+      }
+  };
+  if (use_c && blockIdx.x < P.items) load_c(blockIdx.x, cn);
+  int stage = 0;
+  uint32_t phase = 0;
+  for (long long item = blockIdx.x; item < P.items; item += gridDim.x) {
+    int p, tm, tn;
+    decode_item(P, item, p, tm, tn);
+    if (use_c) {
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) { cv[f][h][0] = cn[f][h][0]; cv[f][h][1] = cn[f][h][1]; }
+      if (item + gridDim.x < P.items) load_c(item + gridDim.x, cn);
+    }
+    if (P.skip && P.skip[p]) continue;
+    const int i0 = tm * TM, j0 = tn * TN;
+    double* dbase = P.o.d + (long long)p * P.o.sd;
+
+    double acc[4][2][2];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc[f][h][0] = acc[f][h][1] = 0.0;
+
+    for (int kc = 0; kc < P.nk; ++kc) {
+      const int kvalid = min(BK, P.k - kc * BK);
+      mbar_wait(&full[stage], phase);
+      const double* sA = smem + (size_t)stage * STAGE;
+      const double* sB = sA + TA::SIZE;
+      if (kvalid == BK) {
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ++ks) {
+          const int l = ks * 4 + t;
+          double av[4], bv[2];
+#pragma unroll
+          for (int f = 0; f < 4; ++f) av[f] = sB[TB::at(jb + f * 8 + g, l)];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) bv[h] = sA[TA::at(ib + h * 8 + g, l)];
+#pragma unroll
+          for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
+        }
+      } else {
+        // Tail chunk: lanes past k contribute exact zeros whatever the stage
+        // holds (pad lanes of panel-major operands are unspecified data).
+        const int ksteps = (kvalid + 3) >> 2;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const int l = ks * 4 + t;
+          const bool in = l < kvalid;
+          double av[4], bv[2];
+#pragma unroll
+          for (int f = 0; f < 4; ++f) av[f] = in ? sB[TB::at(jb + f * 8 + g, l)] : 0.0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) bv[h] = in ? sA[TA::at(ib + h * 8 + g, l)] : 0.0;
+#pragma unroll
+          for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == P.nstages) { stage = 0; phase ^= 1; }
+    }
+
+    // Epilogue: d = alpha*acc + beta*c, masked to the problem and the uplo triangle.
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = i0 + ib + h * 8 + 2 * t, j = j0 + jb + f * 8 + g;
+        if (j >= P.n) continue;
+        double r0 = use_c ? fma(P.alpha, acc[f][h][0], P.beta * cv[f][h][0]) : acc[f][h][0] * P.alpha;
+        double r1 = use_c ? fma(P.alpha, acc[f][h][1], P.beta * cv[f][h][1]) : acc[f][h][1] * P.alpha;
+        bool w0 = i < P.m, w1 = i + 1 < P.m;
+        if (P.uplo == 1) { w0 &= i >= j; w1 &= i + 1 >= j; }
+        if (P.uplo == 2) { w0 &= i <= j; w1 &= i + 1 <= j; }
+        double* dp = dbase + out_off<OUT_PM>(P.o.ldd, i, j);
+        if (w0 && w1 && P.o.vec) {
+          *reinterpret_cast<double2*>(dp) = make_double2(r0, r1);
+        } else {
+          if (w0) dp[0] = r0;
+          if (w1) dbase[out_off<OUT_PM>(P.o.ldd, i + 1, j)] = r1;
+        }
+      }
+  }
+}
+
+template <int OUT_PM>
+__global__ void scale_kernel(OutDesc o, int m, int n, double beta, int uplo, long long total) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long per = (long long)m * n;
+    int p = (int)(e / per);
+    int r = (int)(e - p * per);
+    int i = r % m, j = r / m;
+    if (uplo == 1 && i < j) continue;
+    if (uplo == 2 && i > j) continue;
+    double v = 0.0 * 0.0;  // scale_ab(alpha = 0): 0*0 (+ beta*c) — micro_kernel.hpp:263-273
+    if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, o.c[(long long)p * o.sc + out_off<OUT_PM>(o.ldc, i, j)]));
+    o.d[(long long)p * o.sd + out_off<OUT_PM>(o.ldd, i, j)] = v;
+  }
+}
+
+static int g_sms = 0;
+int num_sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+// ------------------------------------------------------------------ tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// Builds the TMA map of one operand side; returns false when the operand's
+// alignment rules it out (the kernel then uses the cp.async fallback).
+static bool make_map(CUtensorMap* tm, int lay, const OpDesc& d, int xdim, int k, int batch,
+                     int* batched) {
+  auto enc = encode_fn();
+  if (!enc || !d.base) return false;
+  if ((reinterpret_cast<uintptr_t>(d.base) & 15) != 0) return false;
+  if (((long long)d.ld * 8) % 16 != 0) return false;
+  const bool bdim = batch > 1 && d.stride != 0;
+  if (bdim && (d.stride * 8) % 16 != 0) return false;
+  if (xdim <= 0 || k <= 0) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  int rank = 0;
+  switch (lay) {
+    case L_MNC:  // (x, l, p)
+      dims[0] = xdim; dims[1] = k; strides[0] = (cuuint64_t)d.ld * 8;
+      box[0] = LayT<L_MNC>::S; box[1] = BK;
+      rank = 2;
+      break;
+    case L_KC:  // (l, x, p)
+      dims[0] = k; dims[1] = xdim; strides[0] = (cuuint64_t)d.ld * 8;
+      box[0] = LayT<L_KC>::S; box[1] = TM;
+      rank = 2;
+      break;
+    case L_PMX:  // (x%4, l, x/4, p)
+      dims[0] = 4; dims[1] = k; dims[2] = (xdim + 3) / 4;
+      strides[0] = 32; strides[1] = (cuuint64_t)d.ld * 32;
+      box[0] = 4; box[1] = BK; box[2] = TM / 4;
+      rank = 3;
+      break;
+    default:  // L_PML: (l%4, x, l/4, p)
+      dims[0] = 4; dims[1] = xdim; dims[2] = (k + 3) / 4;
+      strides[0] = 32; strides[1] = (cuuint64_t)d.ld * 32;
+      box[0] = 4; box[1] = TM; box[2] = BK / 4;
+      rank = 3;
+      break;
+  }
+  if (bdim) {
+    dims[rank] = batch;
+    strides[rank - 1] = (cuuint64_t)d.stride * 8;
+    box[rank] = 1;
+    ++rank;
+  }
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(d.base), dims,
+                   strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  *batched = bdim;
+  return r == CUDA_SUCCESS;
+}
+
+template <int LA, int LB, int OUT_PM>
+static cudaError_t launch_t(KParams& P, cudaStream_t s) {
+  constexpr int STAGE = LayT<LA>::SIZE + LayT<LB>::SIZE;
+  const size_t stage_bytes = (size_t)STAGE * 8;
+  const size_t budget = 227 * 1024 - 256;
+  int nst = (int)((budget - 16 * 16) / (stage_bytes + 16));
+  nst = std::min(nst, 8);
+  P.nstages = nst;
+  size_t smem = (size_t)nst * stage_bytes + (size_t)nst * 16;
+  auto kern = gemm_tiles_kernel<LA, LB, OUT_PM>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  long long grid = std::min<long long>(P.items, (long long)num_sms());
+  kern<<<(int)grid, NTHREADS, smem, s>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_launch(const GemmLaunch& g, cudaStream_t s) {
+  if (g.batch <= 0 || g.m <= 0 || g.n <= 0) return cudaSuccess;
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  P.a = g.a;
+  P.b = g.b;
+  P.o = g.o;
+  P.m = g.m;
+  P.n = g.n;
+  P.k = g.k;
+  P.alpha = g.alpha;
+  P.beta = g.beta;
+  P.uplo = g.uplo;
+  P.skip = g.skip;
+  P.tiles_m = (g.m + TM - 1) / TM;
+  P.tiles_n = (g.n + TN - 1) / TN;
+  if (g.uplo) {
+    int t = P.tiles_m;  // square (syrk)
+    P.tiles_per_problem = t * (t + 1) / 2;
+  } else {
+    P.tiles_per_problem = P.tiles_m * P.tiles_n;
+  }
+  P.nk = (g.k + BK - 1) / BK;
+  P.items = (long long)g.batch * P.tiles_per_problem;
+  P.nstages = 2;
+  static const bool no_tma = [] {
+    const char* e = getenv("PBGPU_NO_TMA");
+    return e && e[0] == '1';
+  }();
+  if (!no_tma && g.a.bulk) P.tmaA = make_map(&P.tmA, g.lay_a, g.a, g.m, g.k, g.batch, &P.batched_mapA);
+  if (!no_tma && g.b.bulk) P.tmaB = make_map(&P.tmB, g.lay_b, g.b, g.n, g.k, g.batch, &P.batched_mapB);
+  if (!g.out_pm) {
+    if (g.lay_a == L_MNC && g.lay_b == L_MNC) return launch_t<L_MNC, L_MNC, 0>(P, s);
+    if (g.lay_a == L_MNC && g.lay_b == L_KC) return launch_t<L_MNC, L_KC, 0>(P, s);
+    if (g.lay_a == L_KC && g.lay_b == L_MNC) return launch_t<L_KC, L_MNC, 0>(P, s);
+    if (g.lay_a == L_KC && g.lay_b == L_KC) return launch_t<L_KC, L_KC, 0>(P, s);
+  } else {
+    if (g.lay_a == L_PMX && g.lay_b == L_PMX) return launch_t<L_PMX, L_PMX, 1>(P, s);
+    if (g.lay_a == L_PMX && g.lay_b == L_PML) return launch_t<L_PMX, L_PML, 1>(P, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t scale_launch(int out_pm, const OutDesc& o, int m, int n, double beta, int uplo,
+                         int batch, cudaStream_t s) {
+  long long total = (long long)m * n * batch;
+  if (total <= 0) return cudaSuccess;
+  int threads = 256;
+  long long blocks = std::min<long long>((total + threads - 1) / threads, (long long)num_sms() * 16);
+  if (out_pm)
+    scale_kernel<1><<<(int)blocks, threads, 0, s>>>(o, m, n, beta, uplo, total);
+  else
+    scale_kernel<0><<<(int)blocks, threads, 0, s>>>(o, m, n, beta, uplo, total);
+  return cudaGetLastError();
+}
+
+}  // namespace pbg

@@ -1,0 +1,133 @@
+// Internal launcher interface between the host boundary (pbgpu_api.cpp) and
+// the sm_100a kernels.  Plain structs of device pointers and sizes; every
+// launcher is asynchronous on the given stream and returns the launch error.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pbg {
+
+// Operand storage kinds for the tiled DMMA engine (gemm.cu).  x is the
+// operand's row index in the product (i of op(A), j of op(B)^T), l the
+// contraction index.
+enum Lay : int {
+  L_MNC = 0,  // column-major, x contiguous: (x, l) at x + l*ld
+  L_KC = 1,   // column-major, l contiguous: (x, l) at l + x*ld
+  L_PMX = 2,  // panel-major (ps = 4), panels over x: (x/4)*4*cn + l*4 + x%4
+  L_PML = 3,  // panel-major (ps = 4), panels over l: (l/4)*4*cn + x*4 + l%4
+};
+
+struct OpDesc {
+  const double* base = nullptr;  // problem 0
+  long long stride = 0;          // elements between consecutive problems
+  int ld = 0;                    // leading dimension (cm) or panel width cn (pm)
+  int bulk = 0;                  // 1 when every bulk copy is 16-byte aligned
+};
+
+struct OutDesc {
+  const double* c = nullptr;  // source of beta*C (may equal d)
+  double* d = nullptr;
+  long long sc = 0, sd = 0;
+  int ldc = 0, ldd = 0;  // ld (cm) or cn (pm)
+  int vec = 0;           // 1 when 16-byte paired accesses are aligned
+};
+
+struct GemmLaunch {
+  int lay_a = L_MNC, lay_b = L_KC;  // M side (op(A)) and N side (op(B)^T)
+  int out_pm = 0;                   // 0: C/D column-major, 1: panel-major
+  OpDesc a, b;
+  OutDesc o;
+  int m = 0, n = 0, k = 0;
+  double alpha = 1.0, beta = 0.0;
+  int uplo = 0;  // 0 full, 1 lower (i >= j), 2 upper (i <= j)
+  const int* skip = nullptr;  // optional: skip problems with skip[p] != 0
+  int batch = 0;
+};
+cudaError_t gemm_launch(const GemmLaunch& g, cudaStream_t s);
+// d <- beta*c on the (uplo-masked) m x n result; beta == 0 writes +0 without reading c.
+cudaError_t scale_launch(int out_pm, const OutDesc& o, int m, int n, double beta, int uplo,
+                         int batch, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace pbg
+
+namespace pbg {
+
+// Cholesky (dpotrf, in place).  upper = 1 runs the lower algorithm on the
+// transposed storage (factor.hpp:45-99 twin windows).  info[p] receives 0 or
+// the failing column; on failure only the tiles the reference's band
+// schedule would have stored are written (see potrf.cu).
+struct PotrfLaunch {
+  double* a = nullptr;
+  long long stride = 0;
+  int lda = 0, n = 0, upper = 0;
+  int* info = nullptr;
+  int batch = 0;
+};
+cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s);
+
+// LU with partial pivoting (dgetrf, in place).
+struct GetrfLaunch {
+  double* a = nullptr;
+  long long stride = 0;
+  int lda = 0, m = 0, n = 0;
+  int* ipiv = nullptr;
+  long long stride_ipiv = 0;
+  int* info = nullptr;
+  int batch = 0;
+};
+cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s);
+
+// Triangular solve.  Column-major dtrsm (in place on b) or the panel-major
+// trsm_rltn_nd (b -> d, d may alias b).  The effective problem is always a
+// right-side solve X * op(A) = alpha * B over rows of X (Left runs on the
+// transposed B through 'twin' addressing, level3.hpp:300-303).
+struct TrsmLaunch {
+  int pm = 0;                // 0: column-major, 1: panel-major (right/lower/trans/non-unit only)
+  int twin = 0;              // Left side: rows of the effective problem are columns of B
+  int lower = 1, trans = 0;  // flags of the effective (right-side) problem
+  int unit = 0;
+  int mm = 0, nn = 0;  // effective rows (independent) and triangle order
+  double alpha = 1.0;
+  const double* a = nullptr;
+  long long sa = 0;
+  int lda = 0;  // ld (cm) or cn (pm)
+  const double* b = nullptr;
+  long long sb = 0;
+  int ldb = 0;
+  double* d = nullptr;
+  long long sd = 0;
+  int ldd = 0;
+  int* info = nullptr;  // per-problem zero-diagonal report (written before any store)
+  int skip_nonzero = 0; // skip problems whose info is already nonzero (blocked callers)
+  int batch = 0;
+};
+cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s);
+
+// Fused panel-major lower chol(C + A B^T) (syrk_potrf_nd).
+struct SyrkPotrfLaunch {
+  const double *a = nullptr, *b = nullptr, *c = nullptr;
+  double* d = nullptr;
+  long long sa = 0, sb = 0, sc = 0, sd = 0;
+  int cna = 0, cnb = 0, cnc = 0, cnd = 0;
+  int n = 0, k = 0;
+  int* info = nullptr;
+  int batch = 0;
+};
+cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s);
+
+// Variable-size chain (config 5).  layout 0 = column-major, 1 = panel-major.
+struct ChainLaunch {
+  int pm = 0;
+  const int* n = nullptr;
+  const long long* offset = nullptr;
+  double *A = nullptr, *C = nullptr, *B = nullptr;
+  int* info = nullptr;
+  int batch = 0, max_n = 0;
+};
+cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s);
+
+double probe_dmma_tflops();
+
+}  // namespace pbg

@@ -1,0 +1,179 @@
+"""GPU parity: batched dgemm / dsyrk / gemm_nd / syrk_nd through the C ABI vs the oracle."""
+import numpy as np
+import pytest
+
+from helpers import F, ch, ptr, rel_frob, same_bits, tol
+from oracle.binding import dmat, pack, panel_len, unpack
+
+pytestmark = pytest.mark.gpu
+
+
+def _cm_batch(rng, rows, cols, batch, ld=None):
+    ld = ld or rows
+    x = rng.uniform(-1, 1, (batch, cols, ld))  # problem-major, column-major inside
+    return x
+
+
+@pytest.mark.parametrize("ta,tb", [("n", "n"), ("n", "t"), ("t", "n"), ("t", "t")])
+@pytest.mark.parametrize("shape", [(64, 64, 64), (13, 9, 7), (1, 1, 1), (70, 33, 45), (128, 96, 160), (3, 130, 2)])
+def test_dgemm_batched_device(pb, orc, cuda, ta, tb, shape):
+    import torch
+    m, n, k = shape
+    rng = np.random.default_rng(hash((ta, tb, shape)) % 2**32)
+    batch = 5
+    ar, ac = (m, k) if ta == "n" else (k, m)
+    br, bc = (k, n) if tb == "n" else (n, k)
+    A = rng.uniform(-1, 1, (batch, ac, ar))
+    B = rng.uniform(-1, 1, (batch, bc, br))
+    Cm = rng.uniform(-1, 1, (batch, n, m))
+    alpha, beta = 1.5, -0.5
+    dA, dB, dC = (torch.from_numpy(x.copy()).to(cuda) for x in (A, B, Cm))
+    r = pb.dgemm_batched(ta, tb, m, n, k, alpha, dA, ar, ar * ac, dB, br, br * bc, beta, dC, m, m * n, batch)
+    assert r.info == 0 and r.flops == 2 * m * n * k * batch
+    got = dC.cpu().numpy()
+    for p in range(batch):
+        want = F(Cm[p].T)
+        a = F(A[p].T)
+        b = F(B[p].T)
+        orc.dgemm(ch(ta), ch(tb), m, n, k, alpha, ptr(a), ar, ptr(b), br, beta, ptr(want), m)
+        assert rel_frob(got[p].T, want) <= tol(k)
+
+
+def test_dgemm_cfg1_full_batch(pb, orc, cuda):
+    """Config 1 at full size: 16384 problems of 64^3, alpha = beta = 1; every problem checked."""
+    import torch
+    m = n = k = 64
+    batch = 16384
+    g = torch.Generator(device=cuda).manual_seed(7)
+    A = torch.rand((batch, k, m), generator=g, device=cuda, dtype=torch.float64) * 2 - 1
+    B = torch.rand((batch, n, k), generator=g, device=cuda, dtype=torch.float64) * 2 - 1
+    Cm = torch.rand((batch, n, m), generator=g, device=cuda, dtype=torch.float64) * 2 - 1
+    # storage is column-major: C^T = C^T + B^T A^T in the (batch, cols, rows) view
+    want = torch.baddbmm(Cm, B, A)  # fp64 torch reference
+    r = pb.dgemm_batched("n", "n", m, n, k, 1.0, A, m, m * k, B, k, k * n, 1.0, Cm, m, m * n, batch)
+    torch.cuda.synchronize()
+    assert r.ok()
+    err = (torch.linalg.matrix_norm(Cm - want) / torch.linalg.matrix_norm(want)).max().item()
+    assert err <= tol(k)
+
+
+def test_dgemm_host_pointers_single(pb, orc):
+    """The netlib-shaped single call with host buffers (staged through the GPU)."""
+    rng = np.random.default_rng(3)
+    for (m, n, k) in [(13, 9, 7), (64, 64, 64), (5, 1, 33)]:
+        a = F(rng.uniform(-1, 1, (m, k))); b = F(rng.uniform(-1, 1, (k, n))); c = F(rng.uniform(-1, 1, (m, n)))
+        got = c.copy(order="F"); want = c.copy(order="F")
+        r = pb.dgemm("n", "n", m, n, k, 1.0, a, m, b, k, 1.0, got, m)
+        assert r.ok()
+        orc.dgemm(b"n", b"n", m, n, k, 1.0, ptr(a), m, ptr(b), k, 1.0, ptr(want), m)
+        assert rel_frob(got, want) <= tol(k)
+
+
+def test_dgemm_integer_data_bitwise(pb, orc):
+    """Exact-arithmetic inputs (test_gemm.cpp style): results equal the reference bit for bit."""
+    rng = np.random.default_rng(11)
+    for (m, n, k) in [(13, 9, 7), (64, 64, 64), (67, 65, 66)]:
+        for ta in "nt":
+            for tb in "nt":
+                a = F(rng.integers(-4, 5, (m, k) if ta == "n" else (k, m)).astype(float))
+                b = F(rng.integers(-4, 5, (k, n) if tb == "n" else (n, k)).astype(float))
+                c = F(rng.integers(-4, 5, (m, n)).astype(float))
+                got, want = c.copy(order="F"), c.copy(order="F")
+                assert pb.dgemm(ta, tb, m, n, k, 2.0, a, a.shape[0], b, b.shape[0], -1.0, got, m).ok()
+                orc.dgemm(ch(ta), ch(tb), m, n, k, 2.0, ptr(a), a.shape[0], ptr(b), b.shape[0], -1.0, ptr(want), m)
+                assert same_bits(got, want)
+
+
+def test_dgemm_beta_zero_never_reads_c(pb):
+    """test_gemm.cpp:264-286: beta = 0 with NaN in C yields clean results."""
+    rng = np.random.default_rng(5)
+    m, n, k = 21, 17, 9
+    a = F(rng.uniform(-1, 1, (m, k))); b = F(rng.uniform(-1, 1, (k, n)))
+    c = F(np.full((m, n), np.nan))
+    assert pb.dgemm("n", "n", m, n, k, 1.0, a, m, b, k, 0.0, c, m).ok()
+    assert np.isfinite(c).all()
+    assert rel_frob(c, a @ b) <= tol(k)
+
+
+def test_dgemm_quick_returns_and_scale(pb):
+    """test_blas.cpp:121-170: alpha=0/k=0 paths never touch NaN operands."""
+    m, n, k = 5, 4, 3
+    a = F(np.full((m, k), np.nan)); b = F(np.full((k, n), np.nan))
+    c = F(np.array([[1.0 + i + 10.0 * j for j in range(n)] for i in range(m)]))
+    c1 = c.copy(order="F")
+    assert pb.dgemm("n", "n", m, n, k, 0.0, a, m, b, k, 1.0, c1, m).ok() and same_bits(c1, c)
+    c3 = c.copy(order="F")
+    assert pb.dgemm("n", "n", m, n, k, 0.0, a, m, b, k, -2.0, c3, m).ok()
+    assert np.array_equal(c3, -2.0 * c)
+    c4 = c.copy(order="F")
+    assert pb.dgemm("n", "n", m, n, 0, 1.0, a, m, b, k, 0.0, c4, m).ok()
+    assert (c4 == 0.0).all()
+
+
+@pytest.mark.parametrize("s", [4, 8, 12, 28, 64, 100, 132, 320])
+def test_gemm_nd_nt_batched(pb, orc, cuda, s):
+    """Config 2: panel-major D = A B^T + C (non-destructive), checked per problem."""
+    import torch
+    rng = np.random.default_rng(s)
+    batch = 3
+    L = panel_len(s, s)
+    A = rng.uniform(-1, 1, (batch, L)); B = rng.uniform(-1, 1, (batch, L)); Cp = rng.uniform(-1, 1, (batch, L))
+    dA, dB, dC = (torch.from_numpy(x.copy()).to(cuda) for x in (A, B, Cp))
+    dD = torch.full((batch, L), 5.0, device=cuda, dtype=torch.float64)
+    r = pb.gemm_nd_batched("n", "t", s, s, s, 1.0, pb.PanelRef(dA, s, s), L, pb.PanelRef(dB, s, s), L,
+                           1.0, pb.PanelRef(dC, s, s), L, pb.PanelRef(dD, s, s), L, batch)
+    assert r.ok()
+    got = dD.cpu().numpy()
+    for p in range(batch):
+        want = np.full(L, 5.0)
+        orc.gemm_nd(b"n", b"t", s, s, s, 1.0, dmat(A[p], s, s), dmat(B[p], s, s), 1.0, dmat(Cp[p], s, s), dmat(want, s, s))
+        assert rel_frob(unpack(got[p], s, s), unpack(want, s, s)) <= tol(s)
+
+
+def test_gemm_nd_odd_shapes_and_nn(pb, orc):
+    rng = np.random.default_rng(21)
+    for (m, n, k) in [(5, 7, 3), (9, 19, 13), (66, 70, 37)]:
+        for tb in "nt":
+            A = rng.uniform(-1, 1, (m, k)); B = rng.uniform(-1, 1, (k, n) if tb == "n" else (n, k))
+            Cm = rng.uniform(-1, 1, (m, n))
+            ap, bp, cp = pack(A, fill=np.nan), pack(B, fill=np.nan), pack(Cm, fill=np.nan)
+            d = np.full(panel_len(m, n), 9.0); want = d.copy()
+            br, bc = B.shape
+            r = pb.gemm_nd("n", tb, m, n, k, 0.75, pb.PanelRef(ap, m, k), pb.PanelRef(bp, br, bc), -1.25,
+                           pb.PanelRef(cp, m, n), pb.PanelRef(d, m, n))
+            assert r.ok()
+            orc.gemm_nd(b"n", ch(tb), m, n, k, 0.75, dmat(ap, m, k), dmat(bp, br, bc), -1.25, dmat(cp, m, n), dmat(want, m, n))
+            assert rel_frob(unpack(d, m, n), unpack(want, m, n)) <= tol(k)
+            # pad lanes of d are untouched (panel_mat.hpp:8-12)
+            mask = np.ones(panel_len(m, n), bool)
+            i = np.arange(m)[:, None]; j = np.arange(n)[None, :]
+            cn = (n + 3) // 4 * 4
+            mask[(i // 4) * 4 * cn + j * 4 + i % 4] = False
+            assert (d[mask] == 9.0).all()
+
+
+@pytest.mark.parametrize("uplo", ["l", "u"])
+@pytest.mark.parametrize("trans", ["n", "t"])
+def test_dsyrk(pb, orc, uplo, trans):
+    rng = np.random.default_rng(31)
+    for (n, k) in [(11, 6), (64, 64), (100, 37)]:
+        a = F(rng.uniform(-1, 1, (n, k) if trans == "n" else (k, n)))
+        c = F(rng.uniform(-1, 1, (n, n)))
+        got, want = c.copy(order="F"), c.copy(order="F")
+        assert pb.dsyrk(uplo, trans, n, k, 1.25, a, a.shape[0], -0.75, got, n).ok()
+        orc.dsyrk(ch(uplo), ch(trans), n, k, 1.25, ptr(a), a.shape[0], -0.75, ptr(want), n)
+        assert rel_frob(got, want) <= tol(k)
+        tri = np.tril(np.ones((n, n), bool), -1) if uplo == "u" else np.triu(np.ones((n, n), bool), 1)
+        assert same_bits(got[tri], c[tri])  # opposite triangle untouched
+
+
+def test_syrk_nd(pb, orc):
+    rng = np.random.default_rng(41)
+    for (n, k) in [(13, 7), (64, 64), (96, 20)]:
+        A = rng.uniform(-1, 1, (n, k)); Cs = rng.uniform(-1, 1, (n, n))
+        ap, cp = pack(A), pack(Cs)
+        d = np.full(panel_len(n, n), 3.5); want = d.copy()
+        assert pb.syrk_nd(n, k, 1.0, pb.PanelRef(ap, n, k), 1.0, pb.PanelRef(cp, n, n), pb.PanelRef(d, n, n)).ok()
+        orc.syrk_nd(n, k, 1.0, dmat(ap, n, k), 1.0, dmat(cp, n, n), dmat(want, n, n))
+        assert rel_frob(unpack(d, n, n), unpack(want, n, n)) <= tol(k)
+        assert rel_frob(d, want) <= tol(k)  # includes the untouched upper part
