@@ -25,7 +25,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -70,19 +69,16 @@ class ClockSampler:
         self.lines: list[str] = []
 
     def __enter__(self):
+        import tempfile
+        self.path = tempfile.mktemp(prefix="pbgpu_clocks_", suffix=".csv")
         try:
+            self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                                         stdout=self.fh, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
         return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def __exit__(self, *a):
         if self.proc:
@@ -91,6 +87,10 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.fh.close()
+            with open(self.path) as f:
+                self.lines = [ln.strip() for ln in f if ln.strip()]
+            os.unlink(self.path)
 
     def summary(self):
         sm, mx, reasons = [], None, set()

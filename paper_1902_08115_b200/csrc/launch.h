@@ -66,6 +66,9 @@ struct PotrfLaunch {
   int batch = 0;
 };
 cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s);
+// register-resident warp-per-problem Cholesky, n <= 64 (potrf_warp.cu)
+cudaError_t potrf_warp_launch(double* a, long long stride, int lda, int n, int upper, int* info,
+                              int info_offset, int skip_nonzero, int batch, cudaStream_t s);
 
 // LU with partial pivoting (dgetrf, in place).
 struct GetrfLaunch {

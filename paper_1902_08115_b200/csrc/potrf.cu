@@ -20,6 +20,7 @@
 // Larger n is blocked on the host side (pbgpu_api.cpp) over this kernel, the
 // trsm kernel and the DMMA gemm engine.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -200,6 +201,12 @@ constexpr int kPotrfSmemMax = 160;
 
 cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.n <= 0) return cudaSuccess;
+  static const bool no_warp = [] {
+    const char* e = getenv("PBGPU_POTRF_NO_WARP");
+    return e && e[0] == '1';
+  }();
+  if (L.n <= 64 && !no_warp)
+    return potrf_warp_launch(L.a, L.stride, L.lda, L.n, L.upper, L.info, 0, 0, L.batch, s);
   if (L.n <= kPotrfSmemMax)
     return potrf_smem(L.a, L.stride, L.lda, L.n, L.upper, L.info, 0, 0, L.batch, s);
   // Right-looking blocked over 128-column panels: potrf(A11) -> A21 = A21 L11^{-T}
