@@ -69,6 +69,10 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s);
 // register-resident warp-per-problem Cholesky, n <= 64 (potrf_warp.cu)
 cudaError_t potrf_warp_launch(double* a, long long stride, int lda, int n, int upper, int* info,
                               int info_offset, int skip_nonzero, int batch, cudaStream_t s);
+// panel-major (ps = 4) variant; offs/nvec optional (variable batches, ld = round_up(n, 4));
+// zero_fill writes the LowerZero band zeros of syrk_potrf_nd
+cudaError_t potrf_warp_pm_launch(double* a, long long stride, const long long* offs, const int* nvec,
+                                 int cn, int n, int zero_fill, int* info, int batch, cudaStream_t s);
 
 // LU with partial pivoting (dgetrf, in place).
 struct GetrfLaunch {
