@@ -1,0 +1,263 @@
+// Fused panel-major syrk+potrf (syrk_potrf_nd) and the variable-size
+// Riccati-like chain of config 5 (dsyrk -> dpotrf -> dtrsm), plus the batched
+// layout kernels they need (column-major <-> panel-major, gathers).
+//
+//   syrk_potrf_nd (level3.hpp:533-575): n <= 160 runs in ONE kernel — the
+//   pipelined CTA Cholesky with the prologue S = C + A B^T on the tensor cores
+//   and the LowerZero band store; larger n: gemm engine (lower S in D) ->
+//   unpack -> blocked column-major potrf -> pack with the band zeros.
+//
+//   chain (pb_chain_vbatched): problems are split on the host by order.
+//   n <= 160: variable-batch kernels straight on the caller's buffers
+//     column-major: syrk (lower C += A A^T) -> potrf -> trsm X L^T = B
+//     panel-major : fused syrk+potrf (prologue)  -> trsm_rltn
+//   n > 160: problems of equal order are gathered into a strided workspace,
+//   run through the strided batched kernels, and scattered back.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <map>
+#include <vector>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace pbg {
+
+// ------------------------------------------------------------------ layout kernels
+// dst (cm, ld = n) <- src (pm, cn = round_up(n, 4)), per problem (same offsets
+// or strides for both); only the lower triangle when `lower`.
+__global__ void pm_to_cm_kernel(const double* src, long long ss, double* dst, long long sd, int n, int cn,
+                                int lower) {
+  const long long p = blockIdx.y;
+  const double* s = src + p * ss;
+  double* d = dst + p * sd;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int j = e / n, i = e - j * n;
+    if (lower && i < j) continue;
+    d[i + (long long)j * n] = s[(long long)(i >> 2) * 4 * cn + (long long)j * 4 + (i & 3)];
+  }
+}
+// dst (pm) <- src (cm lower, ld = n) with the LowerZero band zeros
+// (strictly-upper entries of each 8-row diagonal band written as 0).
+__global__ void cm_to_pm_band_kernel(const double* src, long long ss, double* dst, long long sd, int n,
+                                     int cn) {
+  const long long p = blockIdx.y;
+  const double* s = src + p * ss;
+  double* d = dst + p * sd;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int j = e / n, i = e - j * n;
+    double v;
+    if (i >= j) v = s[i + (long long)j * n];
+    else if ((i >> 3) == (j >> 3)) v = 0.0;
+    else continue;
+    d[(long long)(i >> 2) * 4 * cn + (long long)j * 4 + (i & 3)] = v;
+  }
+}
+// Square n x n blocks: ws[q] <-> base + offs[idx[q]] (ld preserved).
+__global__ void gather_kernel(const double* base, const long long* offs, const int* idx, double* ws, int nn) {
+  const int q = blockIdx.y;
+  const double* s = base + offs[idx[q]];
+  double* d = ws + (long long)q * nn;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += gridDim.x * blockDim.x) d[e] = s[e];
+}
+__global__ void scatter_kernel(const double* ws, double* base, const long long* offs, const int* idx, int nn) {
+  const int q = blockIdx.y;
+  const double* s = ws + (long long)q * nn;
+  double* d = base + offs[idx[q]];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += gridDim.x * blockDim.x) d[e] = s[e];
+}
+__global__ void scatter_info_kernel(const int* src, const int* idx, int* info, int count) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < count; q += gridDim.x * blockDim.x) info[idx[q]] = src[q];
+}
+
+static dim3 grid2(long long work, int batch) {
+  return dim3((unsigned)std::max<long long>(1, std::min<long long>((work + 255) / 256, 64)), (unsigned)batch);
+}
+
+// ------------------------------------------------------------------ syrk_potrf_nd
+cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
+  if (L.batch <= 0 || L.n <= 0) return cudaSuccess;
+  const bool fused_ok = L.n <= 160 && (L.k == 0 || (L.cna == L.cnb && L.sa == L.sb));
+  if (fused_ok)
+    return syrk_potrf_cta_launch(L.d, L.sd, nullptr, nullptr, L.cnd, L.c, L.sc, L.cnc, L.k ? L.a : nullptr,
+                                 L.k ? L.b : nullptr, L.sa, L.k, L.cna, L.n, 1, 1, L.info, L.batch, s);
+  // Large n: lower S = C + A B^T into D (gemm engine), factor a column-major copy, pack back.
+  cudaError_t e;
+  GemmLaunch g;
+  g.out_pm = 1;
+  g.lay_a = L_PMX;
+  g.lay_b = L_PMX;
+  g.a.base = L.a; g.a.stride = L.sa; g.a.ld = L.cna;
+  g.a.bulk = ((reinterpret_cast<uintptr_t>(L.a) & 15) == 0) && L.sa % 2 == 0;
+  g.b.base = L.b; g.b.stride = L.sb; g.b.ld = L.cnb;
+  g.b.bulk = ((reinterpret_cast<uintptr_t>(L.b) & 15) == 0) && L.sb % 2 == 0;
+  g.o.c = L.c; g.o.d = L.d; g.o.sc = L.sc; g.o.sd = L.sd; g.o.ldc = L.cnc; g.o.ldd = L.cnd;
+  g.o.vec = 0;
+  g.m = g.n = L.n;
+  g.k = L.k;
+  g.alpha = 1.0;
+  g.beta = 1.0;
+  g.uplo = 1;
+  g.batch = L.batch;
+  if (L.k > 0) e = gemm_launch(g, s);
+  else e = scale_launch(1, g.o, L.n, L.n, 1.0, 1, L.batch, s);
+  if (e != cudaSuccess) return e;
+  double* ws = nullptr;
+  const long long nn = (long long)L.n * L.n;
+  e = cudaMallocAsync(&ws, sizeof(double) * nn * L.batch, s);
+  if (e != cudaSuccess) return e;
+  pm_to_cm_kernel<<<grid2(nn, L.batch), 256, 0, s>>>(L.d, L.sd, ws, nn, L.n, L.cnd, 1);
+  PotrfLaunch P;
+  P.a = ws; P.stride = nn; P.lda = L.n; P.n = L.n; P.upper = 0; P.info = L.info; P.batch = L.batch;
+  e = potrf_launch(P, s);
+  if (e == cudaSuccess) {
+    cm_to_pm_band_kernel<<<grid2(nn, L.batch), 256, 0, s>>>(ws, nn, L.d, L.sd, L.n, L.cnd);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(ws, s);
+  return e;
+}
+
+// ------------------------------------------------------------------ chain (cfg 5)
+cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
+  if (L.batch <= 0) return cudaSuccess;
+  cudaError_t e;
+  // The split by order is planned on the host.
+  std::vector<int> nv(L.batch);
+  std::vector<long long> ov(L.batch);
+  if ((e = cudaMemcpyAsync(nv.data(), L.n, sizeof(int) * L.batch, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return e;
+  if ((e = cudaMemcpyAsync(ov.data(), L.offset, sizeof(long long) * L.batch, cudaMemcpyDeviceToHost, s)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  std::vector<int> small;
+  std::map<int, std::vector<int>> big;
+  int nsmall_max = 0;
+  for (int p = 0; p < L.batch; ++p) {
+    if (nv[p] <= 160) {
+      small.push_back(p);
+      nsmall_max = std::max(nsmall_max, nv[p]);
+    } else {
+      big[nv[p]].push_back(p);
+    }
+  }
+  // device scratch: index lists, subset offsets/orders, subset info
+  const size_t nsm = small.size();
+  int *d_idx = nullptr, *d_n = nullptr, *d_info = nullptr;
+  long long* d_off = nullptr;
+  if (nsm) {
+    std::vector<long long> so(nsm);
+    std::vector<int> sn(nsm);
+    for (size_t q = 0; q < nsm; ++q) {
+      so[q] = ov[small[q]];
+      sn[q] = nv[small[q]];
+    }
+    if ((e = cudaMallocAsync(&d_idx, sizeof(int) * nsm, s)) != cudaSuccess) return e;
+    cudaMallocAsync(&d_n, sizeof(int) * nsm, s);
+    cudaMallocAsync(&d_info, sizeof(int) * nsm, s);
+    cudaMallocAsync(&d_off, sizeof(long long) * nsm, s);
+    cudaMemcpyAsync(d_idx, small.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_n, sn.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_off, so.data(), sizeof(long long) * nsm, cudaMemcpyHostToDevice, s);
+    const int bs = (int)nsm;
+    if (!L.pm) {
+      e = syrk_lower_cta_launch(L.C, d_off, d_n, L.A, nsmall_max, 0, d_info, bs, s);
+      if (e == cudaSuccess)
+        e = potrf_cta_launch(L.C, 0, d_off, d_n, 0, nsmall_max, 0, 0, 0, d_info, 0, 0, bs, s);
+    } else {
+      e = syrk_potrf_cta_launch(L.C, 0, d_off, d_n, 0, L.C, 0, 0, L.A, L.A, 0, 1, 0, nsmall_max, 1, 1, d_info,
+                                bs, s);
+    }
+    if (e == cudaSuccess) {
+      TrsmLaunch T;
+      T.pm = L.pm;
+      T.lower = 1; T.trans = 1; T.unit = 0;
+      T.mm = T.nn = nsmall_max;
+      T.alpha = 1.0;
+      T.a = L.C; T.b = L.B; T.d = L.B;
+      T.nvec = d_n; T.offs = d_off;
+      T.info = d_info;
+      T.skip_nonzero = 1;
+      T.batch = bs;
+      e = trsm_launch(T, s);
+    }
+    if (e == cudaSuccess) {
+      scatter_info_kernel<<<std::max(1, (bs + 255) / 256), 256, 0, s>>>(d_info, d_idx, L.info, bs);
+      e = cudaGetLastError();
+    }
+    cudaFreeAsync(d_idx, s);
+    cudaFreeAsync(d_n, s);
+    cudaFreeAsync(d_info, s);
+    cudaFreeAsync(d_off, s);
+    if (e != cudaSuccess) return e;
+  }
+  // large orders: gather -> strided batched chain -> scatter, per distinct n
+  for (auto& kv : big) {
+    const int n = kv.first, cnt = (int)kv.second.size();
+    const long long nn = (long long)n * n;  // n % 4 == 0 in panel-major: pm = cn = n
+    double *wa = nullptr, *wc = nullptr, *wb = nullptr;
+    int *d_i = nullptr, *w_info = nullptr;
+    if ((e = cudaMallocAsync(&wa, sizeof(double) * nn * cnt * 3, s)) != cudaSuccess) return e;
+    wc = wa + nn * cnt;
+    wb = wc + nn * cnt;
+    cudaMallocAsync(&d_i, sizeof(int) * cnt, s);
+    cudaMallocAsync(&w_info, sizeof(int) * cnt, s);
+    cudaMemcpyAsync(d_i, kv.second.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, s);
+    dim3 gg = grid2(nn, cnt);
+    gather_kernel<<<gg, 256, 0, s>>>(L.A, L.offset, d_i, wa, (int)nn);
+    gather_kernel<<<gg, 256, 0, s>>>(L.C, L.offset, d_i, wc, (int)nn);
+    gather_kernel<<<gg, 256, 0, s>>>(L.B, L.offset, d_i, wb, (int)nn);
+    if (!L.pm) {
+      GemmLaunch g;  // dsyrk('l','n'): C += A A^T
+      g.lay_a = g.lay_b = L_MNC;
+      g.a.base = g.b.base = wa; g.a.stride = g.b.stride = nn; g.a.ld = g.b.ld = n; g.a.bulk = g.b.bulk = 1;
+      g.o.c = wc; g.o.d = wc; g.o.sc = g.o.sd = nn; g.o.ldc = g.o.ldd = n; g.o.vec = 1;
+      g.m = g.n = g.k = n;
+      g.alpha = 1.0; g.beta = 1.0; g.uplo = 1; g.batch = cnt;
+      e = gemm_launch(g, s);
+      if (e == cudaSuccess) {
+        PotrfLaunch P;
+        P.a = wc; P.stride = nn; P.lda = n; P.n = n; P.info = w_info; P.batch = cnt;
+        e = potrf_launch(P, s);
+      }
+    } else {
+      SyrkPotrfLaunch S;
+      S.a = S.b = wa; S.c = wc; S.d = wc;
+      S.sa = S.sb = S.sc = S.sd = nn;
+      S.cna = S.cnb = S.cnc = S.cnd = n;
+      S.n = S.k = n;
+      S.info = w_info;
+      S.batch = cnt;
+      e = syrk_potrf_launch(S, s);
+    }
+    if (e == cudaSuccess) {
+      TrsmLaunch T;
+      T.pm = L.pm;
+      T.lower = 1; T.trans = 1; T.unit = 0;
+      T.mm = T.nn = n;
+      T.alpha = 1.0;
+      T.a = wc; T.sa = nn; T.lda = n;
+      T.b = wb; T.sb = nn; T.ldb = n;
+      T.d = wb; T.sd = nn; T.ldd = n;
+      T.info = w_info;
+      T.skip_nonzero = 1;
+      T.batch = cnt;
+      e = trsm_launch(T, s);
+    }
+    if (e == cudaSuccess) {
+      scatter_kernel<<<gg, 256, 0, s>>>(wc, L.C, L.offset, d_i, (int)nn);
+      scatter_kernel<<<gg, 256, 0, s>>>(wb, L.B, L.offset, d_i, (int)nn);
+      scatter_info_kernel<<<std::max(1, (cnt + 255) / 256), 256, 0, s>>>(w_info, d_i, L.info, cnt);
+      e = cudaGetLastError();
+    }
+    cudaFreeAsync(wa, s);
+    cudaFreeAsync(d_i, s);
+    cudaFreeAsync(w_info, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace pbg

@@ -51,10 +51,8 @@ __global__ void __launch_bounds__(256) getrf_smem_kernel(const __grid_constant__
   int* ipiv = P.ipiv + (long long)p * P.sp;
   auto A = [&](int i, int j) -> double& { return sm[i + j * S]; };
 
-  for (int e = tid; e < m * n; e += nthr) {
-    int j = e / m, i = e - j * m;
-    A(i, j) = a[i + (long long)j * P.lda];
-  }
+  stage_cm(sm, S, a, P.lda, 0, m, n, false, tid, nthr);
+  cp_async_wait_all();
   if (tid == 0) first_zero = 0;
   __syncthreads();
 

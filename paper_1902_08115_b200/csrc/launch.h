@@ -69,6 +69,20 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s);
 // register-resident warp-per-problem Cholesky, n <= 64 (potrf_warp.cu)
 cudaError_t potrf_warp_launch(double* a, long long stride, int lda, int n, int upper, int* info,
                               int info_offset, int skip_nonzero, int batch, cudaStream_t s);
+// pipelined left-looking CTA-per-problem Cholesky, n <= 160 (potrf_cta.cu)
+cudaError_t potrf_cta_launch(double* a, long long stride, const long long* offs, const int* nvec, int lda,
+                             int n, int upper, int pm, int zero_fill, int* info, int info_offset,
+                             int skip_nonzero, int batch, cudaStream_t s);
+// same kernel with the prologue S = C + A B^T (A, B n x k, same storage kind as C)
+// (D may differ from C: the kernel stages from c and writes d)
+cudaError_t syrk_potrf_cta_launch(double* d, long long stride_d, const long long* offs, const int* nvec, int ldd,
+                                  const double* c, long long stride_c, int ldc,
+                                  const double* A, const double* B, long long stride_ab, int k, int ldab,
+                                  int n, int pm, int zero_fill, int* info, int batch, cudaStream_t s);
+// variable batch (offs/nvec required): lower C <- C + A A^T only (the chain's dsyrk
+// step), A n x n in the same storage kind, n <= 160
+cudaError_t syrk_lower_cta_launch(double* c, const long long* offs, const int* nvec, const double* A, int nmax,
+                                  int pm, int* info, int batch, cudaStream_t s);
 // panel-major (ps = 4) variant; offs/nvec optional (variable batches, ld = round_up(n, 4));
 // zero_fill writes the LowerZero band zeros of syrk_potrf_nd
 cudaError_t potrf_warp_pm_launch(double* a, long long stride, const long long* offs, const int* nvec,
@@ -109,6 +123,10 @@ struct TrsmLaunch {
   int* info = nullptr;  // per-problem zero-diagonal report (written before any store)
   int skip_nonzero = 0; // skip problems whose info is already nonzero (blocked callers)
   int batch = 0;
+  // variable batches (chain): per-problem order (mm = nn = nvec[p], ld = n or
+  // round_up(n, 4)) and element offsets shared by a, b and d
+  const int* nvec = nullptr;
+  const long long* offs = nullptr;
 };
 cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s);
 

@@ -56,10 +56,8 @@ __global__ void __launch_bounds__(256) potrf_smem_kernel(const __grid_constant__
 
   // ---- load the lower triangle (upper: the transposed storage) ----
   if (!P.upper) {
-    for (int e = tid; e < n * n; e += nthr) {
-      int j = e / n, i = e - j * n;
-      if (i >= j) A(i, j) = a[i + (long long)j * P.lda];
-    }
+    stage_cm(sm, S, a, P.lda, 0, n, n, true, tid, nthr);
+    cp_async_wait_all();
   } else {
     for (int e = tid; e < n * n; e += nthr) {
       int i = e / n, j = e - i * n;  // lower-problem (i, j) = storage (j, i)
@@ -201,12 +199,15 @@ constexpr int kPotrfSmemMax = 160;
 
 cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.n <= 0) return cudaSuccess;
-  static const bool no_warp = [] {
-    const char* e = getenv("PBGPU_POTRF_NO_WARP");
-    return e && e[0] == '1';
+  static const int kernel = [] {  // PBGPU_POTRF_KERNEL: cta (default) | warp | smem
+    const char* e = getenv("PBGPU_POTRF_KERNEL");
+    if (!e) return 0;
+    return e[0] == 'w' ? 1 : (e[0] == 's' ? 2 : 0);
   }();
-  if (L.n <= 64 && !no_warp)
+  if (kernel == 1 && L.n <= 64)
     return potrf_warp_launch(L.a, L.stride, L.lda, L.n, L.upper, L.info, 0, 0, L.batch, s);
+  if (kernel == 0 && L.n <= kPotrfSmemMax)
+    return potrf_cta_launch(L.a, L.stride, nullptr, nullptr, L.lda, L.n, L.upper, 0, 0, L.info, 0, 0, L.batch, s);
   if (L.n <= kPotrfSmemMax)
     return potrf_smem(L.a, L.stride, L.lda, L.n, L.upper, L.info, 0, 0, L.batch, s);
   // Right-looking blocked over 128-column panels: potrf(A11) -> A21 = A21 L11^{-T}
@@ -217,7 +218,7 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     const int w = std::min(nb, L.n - c0), rest = L.n - c0 - w;
     // element (i, j) of the lower problem lives at i + j*lda (lower) or j + i*lda (upper)
     double* a11 = L.a + (long long)c0 + (long long)c0 * L.lda;
-    cudaError_t e = potrf_smem(a11, L.stride, L.lda, w, L.upper, L.info, c0, c0 > 0, L.batch, s);
+    cudaError_t e = potrf_cta_launch(a11, L.stride, nullptr, nullptr, L.lda, w, L.upper, 0, 0, L.info, c0, c0 > 0, L.batch, s);
     if (e != cudaSuccess) return e;
     if (!rest) break;
     TrsmLaunch T;

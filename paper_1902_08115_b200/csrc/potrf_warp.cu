@@ -119,6 +119,42 @@ __device__ __forceinline__ int factor_panel(uint32_t pan, int RS, int rows, int 
   return f;
 }
 
+// One left-looking step k with TA = T - k active 8x8 tiles below/at the
+// diagonal: DMMA update of column block k from the factored panels 0..k-1,
+// then the panel factorization.  Returns 0 or the failing local column.
+template <int T, int TA>
+__device__ __forceinline__ int potrf_step(uint32_t sbase, int k, int lane, int g, int t, uint32_t colb, int n) {
+  const int RS = pstride(T, k);
+  const uint32_t pan = sbase + 8u * panel_base(T, k);
+  if (k > 0) {
+    double acc[TA][2];
+#pragma unroll
+    for (int I = 0; I < TA; ++I) {
+      acc[I][0] = lds64(pan + 8u * ((2 * t) * RS + 8 * I + g));
+      acc[I][1] = lds64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g));
+    }
+    uint32_t pl = sbase + 8u * (8 * k);  // row 8k of panel 0
+    for (int l = 0; l < k; ++l) {
+      const int RL = pstride(T, l);
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const uint32_t col = pl + 8u * ((4 * kk + t) * RL + g);
+        const double bneg = -lds64(col);  // -L(8k+g, 8l+4kk+t)
+#pragma unroll
+        for (int I = 0; I < TA; ++I) dmma(acc[I][0], acc[I][1], lds64(col + 8u * (8 * I)), bneg);
+      }
+      pl += 8u * (8 * RL - 8);  // next panel, same global row 8k
+    }
+#pragma unroll
+    for (int I = 0; I < TA; ++I) {
+      sts64(pan + 8u * ((2 * t) * RS + 8 * I + g), acc[I][0]);
+      sts64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g), acc[I][1]);
+    }
+    __syncwarp();
+  }
+  return factor_panel<(TA > 4)>(pan, RS, 8 * TA, lane, colb, 8 * k, n);
+}
+
 template <int T, int PM>
 __global__ void __launch_bounds__(32 * kWarpsPerCta) potrf_warp_kernel(const __grid_constant__ PotrfWarpArgs P) {
   constexpr int WS = panel_base(T, T) + 8;  // doubles of shared memory per warp (+ broadcast slot)
@@ -182,41 +218,15 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) potrf_warp_kernel(const __g
 
   int fail = 0;
   for (int k = 0; k < TT && P.debug != 1; ++k) {
-    const int tact = TT - k, rows = 8 * tact;
-    const int RS = pstride(T, k);
-    const uint32_t pan = sbase + 8u * panel_base(T, k);
-    // ---- 1. left-looking update of column block k on the tensor cores ----
-    if (k > 0) {
-      double acc[T][2];
-#pragma unroll
-      for (int I = 0; I < T; ++I)
-        if (I < tact) {
-          acc[I][0] = lds64(pan + 8u * ((2 * t) * RS + 8 * I + g));
-          acc[I][1] = lds64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g));
-        }
-      uint32_t pl = sbase + 8u * (8 * k);  // row 8k of panel 0
-      for (int l = 0; l < k; ++l) {
-        const int RL = pstride(T, l);
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          const double bneg = -lds64(pl + 8u * ((4 * kk + t) * RL + g));  // -L(8k+g, 8l+4kk+t)
-#pragma unroll
-          for (int I = 0; I < T; ++I)
-            if (I < tact) dmma(acc[I][0], acc[I][1], lds64(pl + 8u * ((4 * kk + t) * RL + 8 * I + g)), bneg);
-        }
-        pl += 8u * (8 * RL - 8);  // next panel, same global row 8k
-      }
-#pragma unroll
-      for (int I = 0; I < T; ++I)
-        if (I < tact) {
-          sts64(pan + 8u * ((2 * t) * RS + 8 * I + g), acc[I][0]);
-          sts64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g), acc[I][1]);
-        }
-      __syncwarp();
+    int f = 0;
+    switch (TT - k) {  // every step body is fully static in its active tile count
+#define PB_STEP(TA) \
+  case TA:          \
+    if constexpr (TA <= T) f = potrf_step<T, TA>(sbase, k, lane, g, t, colb, n); \
+    break;
+      PB_STEP(1) PB_STEP(2) PB_STEP(3) PB_STEP(4) PB_STEP(5) PB_STEP(6) PB_STEP(7) PB_STEP(8)
+#undef PB_STEP
     }
-    // ---- 2. factor the tall panel ----
-    const int f = rows > 32 ? factor_panel<true>(pan, RS, rows, lane, colb, 8 * k, n)
-                            : factor_panel<false>(pan, RS, rows, lane, colb, 8 * k, n);
     if (f) {
       fail = 8 * k + f;
       break;

@@ -52,15 +52,28 @@ __global__ void __launch_bounds__(256) trsm_kernel(const __grid_constant__ TrsmA
   const int p = blockIdx.x / T.rowblocks, rb = blockIdx.x - p * T.rowblocks;
   if (L.skip_nonzero && L.info[p] != 0) return;
   const int tid = threadIdx.x, nthr = blockDim.x, warp = tid >> 5, lane = tid & 31;
-  const int nn = L.nn, nn8 = T.nn8;
-  const int r0 = rb * TR_R, rows = min(TR_R, L.mm - r0);
-  const double* A = L.a + (long long)p * L.sa;
-  const double* B = L.b + (long long)p * L.sb;
-  double* D = L.d + (long long)p * L.sd;
+  int nn = L.nn, mm = L.mm;
+  int lda = L.lda, ldb = L.ldb, ldd = L.ldd;
+  const double *A, *B;
+  double* D;
+  if (L.nvec) {  // variable batch: square problems at per-problem offsets
+    nn = mm = L.nvec[p];
+    lda = ldb = ldd = PM ? ((nn + 3) & ~3) : nn;
+    A = L.a + L.offs[p];
+    B = L.b + L.offs[p];
+    D = L.d + L.offs[p];
+  } else {
+    A = L.a + (long long)p * L.sa;
+    B = L.b + (long long)p * L.sb;
+    D = L.d + (long long)p * L.sd;
+  }
+  const int nn8 = (nn + 7) & ~7;
+  const int r0 = rb * TR_R, rows = min(TR_R, mm - r0);
+  if (rows <= 0) return;
   double* X = sm;                       // TR_SX x nn8
   double* Pn = sm + (size_t)TR_SX * nn8;  // TR_SP x nn8: rows c0..c0+7 of op(A)
   auto opA = [&](int l, int c) -> double {
-    return L.trans ? A[aoff<PM>(L.lda, c, l)] : A[aoff<PM>(L.lda, l, c)];
+    return L.trans ? A[aoff<PM>(lda, c, l)] : A[aoff<PM>(lda, l, c)];
   };
 
   // Zero-diagonal test before any store: smallest exactly-zero index.
@@ -68,7 +81,7 @@ __global__ void __launch_bounds__(256) trsm_kernel(const __grid_constant__ TrsmA
   __syncthreads();
   if (!L.unit)
     for (int i = tid; i < nn; i += nthr)
-      if (A[aoff<PM>(L.lda, i, i)] == 0.0) atomicMin(&sh_zero, i + 1);
+      if (A[aoff<PM>(lda, i, i)] == 0.0) atomicMin(&sh_zero, i + 1);
   __syncthreads();
   if (sh_zero != 0x7fffffff) {
     if (rb == 0 && tid == 0 && !L.skip_nonzero && L.info) L.info[p] = sh_zero;
@@ -80,7 +93,7 @@ __global__ void __launch_bounds__(256) trsm_kernel(const __grid_constant__ TrsmA
     int c, r;
     if (!PM && L.twin) { r = e / nn8; c = e - r * nn8; } else { c = e / TR_R; r = e - c * TR_R; }
     double v = 0.0;
-    if (r < rows && c < nn) v = L.alpha * B[xoff<PM>(L.twin, L.ldb, r0 + r, c)];
+    if (r < rows && c < nn) v = L.alpha * B[xoff<PM>(L.twin, ldb, r0 + r, c)];
     X[r + c * TR_SX] = v;
   }
 
@@ -154,12 +167,12 @@ __global__ void __launch_bounds__(256) trsm_kernel(const __grid_constant__ TrsmA
   if (!PM && L.twin) {  // storage columns are rows of X: coalesce over c
     for (int e = tid; e < rows * nn; e += nthr) {
       int r = e / nn, c = e - r * nn;
-      D[xoff<0>(1, L.ldd, r0 + r, c)] = X[r + c * TR_SX];
+      D[xoff<0>(1, ldd, r0 + r, c)] = X[r + c * TR_SX];
     }
   } else {
     for (int e = tid; e < rows * nn; e += nthr) {
       int c = e / rows, r = e - c * rows;
-      D[xoff<PM>(0, L.ldd, r0 + r, c)] = X[r + c * TR_SX];
+      D[xoff<PM>(0, ldd, r0 + r, c)] = X[r + c * TR_SX];
     }
   }
   if (rb == 0 && tid == 0 && !L.skip_nonzero && L.info) L.info[p] = 0;
