@@ -290,6 +290,12 @@ def run_gpu_arm(args, ws, rank, local):
                          stream=stream)
 
     with ClockSampler(local) as clk:
+        # clock soak: keep the same workload running ~0.6 s so nvidia-smi (100 ms
+        # period) samples the clocks under this load; then W warm-up + K timed steps
+        t_end = time.perf_counter() + 0.6
+        while time.perf_counter() < t_end:
+            step()
+            torch.cuda.synchronize()
         ms_total = time_device(step, args.steps, args.warmup, stream, ws)
     ms_total = max_over_ranks(ms_total, ws)
     ms_step = ms_total / args.steps
