@@ -119,6 +119,47 @@ __device__ __forceinline__ int cta_factor_panel(uint32_t pan, int RS, int rows, 
   return f;
 }
 
+// Update warp: column block k1's tiles I = uw + NU*s (s < NS) accumulate
+// -sum_l L(I, l) L(k1, l)^T over l < k1 (panel k1-1 after its publication),
+// then go back to shared memory.  Returns true when the panel warp reported
+// a failure (the block is then left untouched).
+template <int T, int NU, int NS>
+__device__ __forceinline__ bool cta_update_block(uint32_t sbase, int k1, int uw, int g, int t, const int* sh_fail) {
+  constexpr int NTH = 32 * (NU + 1);
+  const int RS = cta_pstride(T, k1);
+  const uint32_t pan = sbase + 8u * cta_pbase(T, k1);
+  double acc[NS > 0 ? NS : 1][2];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int I = uw + NU * s;
+    acc[s][0] = lds64(pan + 8u * ((2 * t) * RS + 8 * I + g));
+    acc[s][1] = lds64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g));
+  }
+  uint32_t pl = sbase + 8u * (8 * k1 + g);  // row 8*k1 + g of panel 0
+  for (int l = 0; l < k1; ++l) {
+    if (l == k1 - 1) {
+      named_sync(1, NTH);  // wait for panel k1-1
+      if (*(volatile const int*)sh_fail) return true;
+    }
+    const int RL = cta_pstride(T, l);
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t col = pl + 8u * ((4 * kk + t) * RL);
+      const double bneg = -lds64(col);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) dmma(acc[s][0], acc[s][1], lds64(col + 8u * (8 * (uw + NU * s))), bneg);
+    }
+    pl += 8u * (8 * RL - 8);
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int I = uw + NU * s;
+    sts64(pan + 8u * ((2 * t) * RS + 8 * I + g), acc[s][0]);
+    sts64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g), acc[s][1]);
+  }
+  return false;
+}
+
 template <int T, int NU, int PM>
 __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_constant__ PotrfCtaArgs P) {
   constexpr int NTH = 32 * (NU + 1);
@@ -126,6 +167,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   constexpr int SLOTS = (T + NU - 1) / NU;       // tiles per update warp
   extern __shared__ __align__(16) double sm[];
   __shared__ int sh_fail;
+  __shared__ __align__(8) uint64_t sh_bar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const long long p = blockIdx.x;
   if (P.skip_nonzero && P.info[p] != 0) return;
@@ -142,25 +184,45 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   // ---- stage the lower triangle (panel k: rows 8k.. of columns 8k..8k+7) ----
   const double* sa = P.src ? P.src + (P.offs ? P.offs[p] : p * P.src_stride) : a;
   const long long sld = P.src ? (P.nvec ? lda : P.src_ld) : lda;
-  const bool pairs = !PM && !P.upper && (sld % 2 == 0) && ((reinterpret_cast<uintptr_t>(sa) & 15) == 0);
-  for (int k = 0; k < TT; ++k) {
-    double* pan = sm + cta_pbase(T, k);
-    const int RS = cta_pstride(T, k), r0 = 8 * k, nr = min(n, 8 * TT) - r0;
-    if (pairs) {
-      const int np = (nr + 1) >> 1, tot = 8 * np;
-      const double* src = sa + r0 + (long long)r0 * sld;
-      for (int e = tid; e < tot; e += NTH) {
-        const int c = e / np, q = e - c * np;
-        if (r0 + c >= n) continue;
-        if (2 * q + 1 < nr) cp_async16(&pan[c * RS + 2 * q], src + c * sld + 2 * q);
-        else cp_async8(&pan[c * RS + 2 * q], src + c * sld + 2 * q, true);
-      }
-    } else {
-      const int tot = 8 * nr;
-      for (int e = tid; e < tot; e += NTH) {
-        const int c = e / nr, r = e - c * nr, row = r0 + r, col = r0 + c;
-        const bool v = col < n && row >= col;
-        cp_async8(&pan[c * RS + r], v ? sa + cta_eoff<PM>(P.upper, sld, row, col) : sa, v);
+  const bool bulk = !PM && !P.upper && (sld % 2 == 0) && ((reinterpret_cast<uintptr_t>(sa) & 15) == 0) &&
+                    (n % 2 == 0);
+  if (bulk) {
+    // one TMA bulk copy per column (rows 8k..n-1 of column col, k = col/8)
+    if (tid == 0) {
+      mbar_init(&sh_bar, 1);
+      fence_mbar_init();
+      uint32_t bytes = 0;
+      for (int k = 0; k < TT; ++k) bytes += 8u * (uint32_t)min(8, n - 8 * k) * (uint32_t)(n - 8 * k);
+      mbar_arrive_expect_tx(&sh_bar, bytes);
+    }
+    __syncthreads();
+    for (int col = tid; col < n; col += NTH) {
+      const int k = col >> 3, c = col & 7, r0 = 8 * k;
+      bulk_g2s(sm + cta_pbase(T, k) + c * cta_pstride(T, k), sa + r0 + (long long)col * sld,
+               8u * (uint32_t)(n - r0), &sh_bar);
+    }
+    mbar_wait(&sh_bar, 0);
+  } else {
+    const bool pairs = !PM && !P.upper && (sld % 2 == 0) && ((reinterpret_cast<uintptr_t>(sa) & 15) == 0);
+    for (int k = 0; k < TT; ++k) {
+      double* pan = sm + cta_pbase(T, k);
+      const int RS = cta_pstride(T, k), r0 = 8 * k, nr = min(n, 8 * TT) - r0;
+      if (pairs) {
+        const int np = (nr + 1) >> 1, tot = 8 * np;
+        const double* src = sa + r0 + (long long)r0 * sld;
+        for (int e = tid; e < tot; e += NTH) {
+          const int c = e / np, q = e - c * np;
+          if (r0 + c >= n) continue;
+          if (2 * q + 1 < nr) cp_async16(&pan[c * RS + 2 * q], src + c * sld + 2 * q);
+          else cp_async8(&pan[c * RS + 2 * q], src + c * sld + 2 * q, true);
+        }
+      } else {
+        const int tot = 8 * nr;
+        for (int e = tid; e < tot; e += NTH) {
+          const int c = e / nr, r = e - c * nr, row = r0 + r, col = r0 + c;
+          const bool v = col < n && row >= col;
+          cp_async8(&pan[c * RS + r], v ? sa + cta_eoff<PM>(P.upper, sld, row, col) : sa, v);
+        }
       }
     }
   }
@@ -226,47 +288,20 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
     // ------------------------------------------------------------ update warps
     const int uw = warp - 1;
     for (int k1 = 1; k1 < TT; ++k1) {  // block to update; panel k1-1 is being factored
-      const int ta = TT - k1, RS = cta_pstride(T, k1);
-      const uint32_t pan = sbase + 8u * cta_pbase(T, k1);
-      double acc[SLOTS][2];
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s) {
-        const int I = uw + NU * s;
-        if (I < ta) {
-          acc[s][0] = lds64(pan + 8u * ((2 * t) * RS + 8 * I + g));
-          acc[s][1] = lds64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g));
-        }
+      const int ta = TT - k1;
+      const int ns = uw < ta ? (ta - uw + NU - 1) / NU : 0;  // this warp's active tiles
+      bool stop = false;
+      switch (ns) {  // every case fully static: no predicated tensor-core instructions
+#define PB_UPD(NSV) \
+  case NSV:         \
+    if constexpr (NSV <= SLOTS) stop = cta_update_block<T, NU, NSV>(sbase, k1, uw, g, t, &sh_fail); \
+    break;
+        PB_UPD(0) PB_UPD(1) PB_UPD(2) PB_UPD(3) PB_UPD(4) PB_UPD(5) PB_UPD(6) PB_UPD(7)
+#undef PB_UPD
       }
-      uint32_t pl = sbase + 8u * (8 * k1);  // row 8*k1 of panel 0
-      for (int l = 0; l < k1; ++l) {
-        if (l == k1 - 1) {
-          named_sync(1, NTH);  // wait for panel k1-1
-          if (sh_fail) {
-            fail = 1;
-            break;
-          }
-        }
-        const int RL = cta_pstride(T, l);
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          const uint32_t col = pl + 8u * ((4 * kk + t) * RL + g);
-          const double bneg = -lds64(col);
-#pragma unroll
-          for (int s = 0; s < SLOTS; ++s) {
-            const int I = uw + NU * s;
-            if (I < ta) dmma(acc[s][0], acc[s][1], lds64(col + 8u * (8 * I)), bneg);
-          }
-        }
-        pl += 8u * (8 * RL - 8);
-      }
-      if (fail) break;
-#pragma unroll
-      for (int s = 0; s < SLOTS; ++s) {
-        const int I = uw + NU * s;
-        if (I < ta) {
-          sts64(pan + 8u * ((2 * t) * RS + 8 * I + g), acc[s][0]);
-          sts64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g), acc[s][1]);
-        }
+      if (stop) {
+        fail = 1;
+        break;
       }
       named_sync(2, NTH);  // block k1 ready for the panel warp
     }
@@ -283,17 +318,37 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   }
   const int ncols = fail ? band_cols : n;
   const bool zf = P.zero_fill;
-  for (int kb = 0; kb * 8 < ncols; ++kb) {
-    const uint32_t pb = sbase + 8u * cta_pbase(T, kb);
-    const int RS = cta_pstride(T, kb), r0 = 8 * kb, rows = min(n, 8 * TT) - r0;
-    for (int e = tid; e < 8 * rows; e += NTH) {
-      const int c = e / rows, r = e - c * rows, row = r0 + r, col = r0 + c;
-      if (col >= ncols || row >= n) continue;
+  if (!PM && !P.upper && !zf && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (n % 2 == 0)) {
+    // one TMA bulk store per column for the 16-byte aligned part of rows [col, rlim);
+    // an odd first row goes alone (its pair partner is in the opposite triangle)
+    fence_proxy_async();
+    for (int col = tid; col < ncols; col += NTH) {
+      const int kb = col >> 3, c = col & 7, r0 = 8 * kb;
       const int rlim = fail ? (col >= band_cols ? band_lo : band_lo + 8) : n;
-      if (row >= rlim) continue;
-      if (row < col && !zf) continue;
-      const double v = row >= col ? lds64(pb + 8u * (c * RS + r)) : 0.0;
-      a[cta_eoff<PM>(P.upper, lda, row, col)] = v;
+      const uint32_t pc = sbase + 8u * (cta_pbase(T, kb) + c * cta_pstride(T, kb) - r0);  // + 8*row
+      double* dst = a + (long long)col * lda;
+      int re = col;
+      if ((col & 1) && col < rlim) {
+        dst[col] = lds64(pc + 8u * col);
+        re = col + 1;
+      }
+      if (rlim > re) bulk_s2g(dst + re, pc + 8u * re, 8u * (uint32_t)(rlim - re));
+    }
+    bulk_commit();
+    bulk_wait_read0();
+  } else {
+    for (int kb = 0; kb * 8 < ncols; ++kb) {
+      const uint32_t pb = sbase + 8u * cta_pbase(T, kb);
+      const int RS = cta_pstride(T, kb), r0 = 8 * kb, rows = min(n, 8 * TT) - r0;
+      for (int e = tid; e < 8 * rows; e += NTH) {
+        const int c = e / rows, r = e - c * rows, row = r0 + r, col = r0 + c;
+        if (col >= ncols || row >= n) continue;
+        const int rlim = fail ? (col >= band_cols ? band_lo : band_lo + 8) : n;
+        if (row >= rlim) continue;
+        if (row < col && !zf) continue;
+        const double v = row >= col ? lds64(pb + 8u * (c * RS + r)) : 0.0;
+        a[cta_eoff<PM>(P.upper, lda, row, col)] = v;
+      }
     }
   }
   if (tid == 0) P.info[p] = fail ? fail + P.info_offset : 0;
