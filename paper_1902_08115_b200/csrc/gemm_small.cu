@@ -1,0 +1,164 @@
+// Small-size branch of the batched panel-major gemm_nd (level3.hpp:360-403),
+// D = alpha * A * B^T + beta * C with m = n = k = s <= 32, s % 4 == 0, ps = 4,
+// problems packed back to back (stride = s*s, pm = cn = s).
+//
+// The paper's size switch (gemm.hpp:190-204) picks a different algorithm for
+// tiny operands; on the GPU the 64x64-tile engine would waste most of every
+// tile and every TMA box at these sizes.  Here a persistent CTA streams
+// CHUNKS of G consecutive problems: A, B and C of a chunk are each one
+// contiguous TMA bulk copy into a double-buffered shared-memory ring, every
+// warp computes whole problems with FP64 tensor-core DMMA m8n8k4 straight
+// from the panel-major layout (fragment loads are conflict-free because a
+// 4-row panel column is 32 contiguous bytes), D overwrites C in shared memory
+// and leaves as one bulk store per chunk.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace pbg {
+
+struct SmallArgs {
+  const double *a, *b, *c;
+  double* d;
+  double alpha, beta;
+  long long batch;
+  int s, G, nchunks;
+};
+
+constexpr int SM_WARPS = 4;
+
+template <int T>  // T = ceil(s / 8) row/column tiles per problem
+__global__ void __launch_bounds__(32 * SM_WARPS) gemm_small_kernel(const __grid_constant__ SmallArgs P) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int s = P.s, ss = s * s, G = P.G;
+  const bool use_c = P.beta != 0.0;
+  double* buf[2] = {sm, sm + 3 * (size_t)G * ss};
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int chunk, int slot) {
+    const long long p0 = (long long)chunk * G;
+    const int np = (int)(P.batch - p0 < G ? P.batch - p0 : G);
+    const uint32_t bytes = 8u * (uint32_t)np * ss;
+    double* sA = buf[slot];
+    mbar_arrive_expect_tx(&full[slot], use_c ? 3 * bytes : 2 * bytes);
+    bulk_g2s(sA, P.a + p0 * ss, bytes, &full[slot]);
+    bulk_g2s(sA + (size_t)G * ss, P.b + p0 * ss, bytes, &full[slot]);
+    if (use_c) bulk_g2s(sA + 2 * (size_t)G * ss, P.c + p0 * ss, bytes, &full[slot]);
+  };
+  int it = 0;
+  int chunk = blockIdx.x;
+  if (tid == 0 && chunk < P.nchunks) issue(chunk, 0);
+  for (; chunk < P.nchunks; chunk += gridDim.x, ++it) {
+    const int slot = it & 1;
+    const int next = chunk + gridDim.x;
+    // the other slot's bulk store (previous chunk) must have drained before reuse
+    if (tid == 0) {
+      bulk_wait_read0();
+      if (next < P.nchunks) issue(next, slot ^ 1);
+    }
+    mbar_wait(&full[slot], (it >> 1) & 1);
+    const long long p0 = (long long)chunk * G;
+    const int np = (int)(P.batch - p0 < G ? P.batch - p0 : G);
+    const double* sA = buf[slot];
+    const double* sB = sA + (size_t)G * ss;
+    double* sC = buf[slot] + 2 * (size_t)G * ss;  // D is written here, over C
+    for (int q = warp; q < np; q += SM_WARPS) {
+      const double* A = sA + (size_t)q * ss;
+      const double* B = sB + (size_t)q * ss;
+      double* Cq = sC + (size_t)q * ss;
+      double acc[T][T][2];
+#pragma unroll
+      for (int I = 0; I < T; ++I)
+#pragma unroll
+        for (int J = 0; J < T; ++J) acc[I][J][0] = acc[I][J][1] = 0.0;
+      for (int l0 = 0; l0 < s; l0 += 4) {
+        double fa[T], fb[T];
+#pragma unroll
+        for (int I = 0; I < T; ++I) {
+          // row 8I+g, column l0+t of a panel-major s x s operand; rows past s
+          // read the neighbour's data and only feed discarded outputs
+          const int r = 8 * I + g;
+          const long long off = (long long)(r >> 2) * 4 * s + (l0 + t) * 4 + (r & 3);
+          fa[I] = A[off];
+          fb[I] = B[off];
+        }
+#pragma unroll
+        for (int I = 0; I < T; ++I)
+#pragma unroll
+          for (int J = 0; J < T; ++J) dmma(acc[I][J][0], acc[I][J][1], fa[I], fb[J]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int I = 0; I < T; ++I)
+#pragma unroll
+        for (int J = 0; J < T; ++J)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+            if (r < s && c < s) {
+              const long long off = (long long)(r >> 2) * 4 * s + c * 4 + (r & 3);
+              const double v = use_c ? fma(P.alpha, acc[I][J][e], P.beta * Cq[off]) : P.alpha * acc[I][J][e];
+              Cq[off] = v;
+            }
+          }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async();
+      bulk_s2g(P.d + p0 * ss, smem_u32(sC), 8u * (uint32_t)np * ss);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_read0();
+}
+
+template <int T>
+static cudaError_t small_t(SmallArgs& P, cudaStream_t st) {
+  const size_t smem = 2 * 3 * (size_t)P.G * P.s * P.s * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_small_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         110 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = (int)std::min<long long>(P.nchunks, 2LL * num_sms());
+  gemm_small_kernel<T><<<grid, 32 * SM_WARPS, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+bool gemm_small_ok(int s, const double* a, const double* b, const double* c, const double* d, long long sa,
+                   long long sb, long long sc, long long sd, int cna, int cnb, int cnc, int cnd) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const long long ss = (long long)s * s;
+  return s > 0 && s <= 32 && s % 4 == 0 && sa == ss && sb == ss && sc == ss && sd == ss && cna == s &&
+         cnb == s && cnc == s && cnd == s && al(a) && al(b) && al(c) && al(d);
+}
+
+cudaError_t gemm_small_launch(int s, double alpha, const double* a, const double* b, double beta,
+                              const double* c, double* d, long long batch, cudaStream_t st) {
+  SmallArgs P;
+  P.a = a; P.b = b; P.c = c; P.d = d;
+  P.alpha = alpha; P.beta = beta;
+  P.batch = batch;
+  P.s = s;
+  // chunk: ~32 KB per operand per stage, two stages of A, B, C -> <= ~192 KB... keep two CTAs/SM
+  P.G = std::max(1, 2048 / (s * s));
+  P.nchunks = (int)((batch + P.G - 1) / P.G);
+  switch ((s + 7) / 8) {
+    case 1: return small_t<1>(P, st);
+    case 2: return small_t<2>(P, st);
+    case 3: return small_t<3>(P, st);
+    case 4: return small_t<4>(P, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace pbg

@@ -16,6 +16,7 @@
 // Larger problems are blocked on the host side over this kernel (tall
 // panels), a row-swap kernel, the trsm kernel and the DMMA gemm engine.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -212,6 +213,12 @@ static bool fits_smem(int m, int n) {
 
 cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.m <= 0 || L.n <= 0) return cudaSuccess;
+  static const bool legacy = [] {
+    const char* e = getenv("PBGPU_GETRF_KERNEL");
+    return e && e[0] == 's';
+  }();
+  if (fits_smem(L.m, L.n) && !legacy && L.m <= 224)
+    return getrf_cta_launch(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, 0, 0, L.batch, s);
   if (fits_smem(L.m, L.n))
     return getrf_smem(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, 0, 0, L.batch, s);
   // Blocked right-looking LU over tall panels of nb columns.
@@ -225,8 +232,11 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
     const int mm = L.m - j0;
     double* panel = L.a + (long long)j0 + (long long)j0 * L.lda;
     // 1. factor the tall panel rows j0.., cols j0..j0+jb (pivots offset by j0)
-    cudaError_t e = getrf_smem(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info,
-                               j0, j0 > 0, L.batch, s);
+    cudaError_t e = (!legacy && mm <= 224)
+                        ? getrf_cta_launch(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info, j0,
+                                           j0 > 0, L.batch, s)
+                        : getrf_smem(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info, j0,
+                                     j0 > 0, L.batch, s);
     if (e != cudaSuccess) return e;
     // 2. apply the panel's interchanges to the columns left and right of it
     dim3 grid(std::max(1, (std::max(j0, L.n - j0 - jb) + 127) / 128), L.batch);

@@ -50,6 +50,12 @@ cudaError_t scale_launch(int out_pm, const OutDesc& o, int m, int n, double beta
 
 int num_sms();
 
+// small-size panel-major NT gemm (s <= 32, packed problems): gemm_small.cu
+bool gemm_small_ok(int s, const double* a, const double* b, const double* c, const double* d, long long sa,
+                   long long sb, long long sc, long long sd, int cna, int cnb, int cnc, int cnd);
+cudaError_t gemm_small_launch(int s, double alpha, const double* a, const double* b, double beta,
+                              const double* c, double* d, long long batch, cudaStream_t st);
+
 }  // namespace pbg
 
 namespace pbg {
@@ -99,6 +105,9 @@ struct GetrfLaunch {
   int batch = 0;
 };
 cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s);
+// pipelined CTA-per-problem LU for shared-memory-resident problems (getrf_cta.cu)
+cudaError_t getrf_cta_launch(double* a, long long stride, int lda, int m, int n, int* ipiv, long long sp,
+                             int* info, int piv_offset, int keep_info, int batch, cudaStream_t s);
 
 // Triangular solve.  Column-major dtrsm (in place on b) or the panel-major
 // trsm_rltn_nd (b -> d, d may alias b).  The effective problem is always a

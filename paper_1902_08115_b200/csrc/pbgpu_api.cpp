@@ -712,6 +712,12 @@ static int gemm_nd_impl(bool batched, char transa, char transb, int m, int n, in
                          o.ldc = c.cn; o.ldd = d.cn;
                          o.vec = aligned16(o.c) && aligned16(o.d) && sc % 2 == 0 && sd % 2 == 0;
                          if (scale_only) return scale_launch(1, o, m, n, beta, 0, nb, s);
+                         // size switch (gemm.hpp:190-204): tiny square NT problems stream in chunks
+                         if (tb == 1 && m == n && n == k && !alias &&
+                             gemm_small_ok(m, (const double*)p[0], (const double*)p[1], o.c, o.d, sa, sb, sc, sd,
+                                           a.cn, b.cn, c.cn, d.cn))
+                           return gemm_small_launch(m, alpha, (const double*)p[0], (const double*)p[1], beta, o.c,
+                                                    o.d, nb, s);
                          GemmLaunch g;
                          g.out_pm = 1;
                          g.lay_a = L_PMX;
