@@ -149,7 +149,7 @@ cudaError_t gemm_small_launch(int s, double alpha, const double* a, const double
   P.alpha = alpha; P.beta = beta;
   P.batch = batch;
   P.s = s;
-  // chunk: ~32 KB per operand per stage, two stages of A, B, C -> <= ~192 KB... keep two CTAs/SM
+  // chunk: <= 16 KB per operand; two stages of A, B, C = 96 KB, two CTAs per SM
   P.G = std::max(1, 2048 / (s * s));
   P.nchunks = (int)((batch + P.G - 1) / P.G);
   switch ((s + 7) / 8) {

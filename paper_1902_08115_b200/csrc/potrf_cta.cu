@@ -64,58 +64,102 @@ __device__ __forceinline__ long long cta_eoff(int upper, long long ld, int r, in
   return upper ? (long long)c + r * ld : (long long)r + c * ld;
 }
 
+// PB_TRACE (tools/potrf_trace.cu only): per-CTA clock64 stamps of the phases
+#ifdef PB_TRACE
+__device__ long long pb_trace[256][64];
+#define PB_STAMP(slot) \
+  if ((blockIdx.x & 31) == 0 && (blockIdx.x >> 5) < 256 && (slot) < 64) pb_trace[blockIdx.x >> 5][slot] = clock64();
+#else
+#define PB_STAMP(slot)
+#endif
+
 __device__ __forceinline__ void named_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
 
 // Panel warp: factor the (rows x 8) panel in place; lane owns rows lane + 32 q.
-template <int R>
-__device__ __forceinline__ int cta_factor_panel(uint32_t pan, int RS, int rows, int lane, uint32_t colb,
-                                                int gcol0, int n) {
-  const unsigned FULL = 0xffffffffu;
-  double x[R][8];
-#pragma unroll
-  for (int q = 0; q < R; ++q)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) x[q][c] = (lane + 32 * q < rows) ? lds64(pan + 8u * (c * RS + lane + 32 * q)) : 0.0;
+// Every lane factors the 8x8 diagonal block D redundantly in registers, so a
+// column step is rsqrt -> scale -> update with no shuffle or shared-memory
+// round trip on the dependency chain; the lane's own rows follow the same
+// recurrence (the rows of D itself come out bitwise equal to D's entries,
+// the strict upper part of the block is scratch).
+// Slow twin for the rare panels whose pivots are denormal or +inf (where the
+// branch-free rsqrt_nb is not exact): CUDA rsqrt(), rows straight in shared
+// memory, early exit at a failed column.
+__device__ __noinline__ int cta_factor_panel_exact(uint32_t pan, int RS, int rows, int lane, int gcol0, int n) {
   int f = 0;
-#pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const double piv = __shfl_sync(FULL, x[0][c], c);
+    const double piv = lds64(pan + 8u * (c * RS + c));
+    __syncwarp();
     if (gcol0 + c < n && piv <= 0.0) {
       f = c + 1;
       break;
     }
     const double inv = rsqrt(piv);
-    if (lane == c) x[0][c] = piv * inv;
-    else if (lane > c) x[0][c] *= inv;
-#pragma unroll
-    for (int q = 1; q < R; ++q) x[q][c] *= inv;
-    if (c < 7) {
-      if (lane > c && lane < 8) sts64(colb + 8u * lane, x[0][c]);
-      __syncwarp();
-      double fc[8];
-#pragma unroll
-      for (int c2 = (c + 1) & ~1; c2 < 8; c2 += 2) {
-        double2 v;
-        asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(colb + 8u * c2));
-        fc[c2] = v.x;
-        fc[c2 + 1] = v.y;
-      }
-#pragma unroll
-      for (int c2 = c + 1; c2 < 8; ++c2) {
-        if (lane >= c2) x[0][c2] -= x[0][c] * fc[c2];
-#pragma unroll
-        for (int q = 1; q < R; ++q) x[q][c2] -= x[q][c] * fc[c2];
-      }
-      __syncwarp();
+    for (int r = c + lane; r < rows; r += 32) {
+      const uint32_t a = pan + 8u * (c * RS + r);
+      sts64(a, r == c ? piv * inv : lds64(a) * inv);
     }
+    __syncwarp();
+    for (int c2 = c + 1; c2 < 8; ++c2) {
+      const double l = lds64(pan + 8u * (c * RS + c2));
+      for (int r = c2 + lane; r < rows; r += 32) {
+        const uint32_t a = pan + 8u * (c2 * RS + r);
+        sts64(a, lds64(a) - lds64(pan + 8u * (c * RS + r)) * l);
+      }
+    }
+    __syncwarp();
   }
+  return f;
+}
+
+template <int R>
+__device__ __forceinline__ int cta_factor_panel(uint32_t pan, int RS, int rows, int lane, int gcol0, int n) {
+  double x[R][8];
+  double D[8][8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+#pragma unroll
+    for (int i = c & ~1; i < 8; i += 2) {
+      double2 v;
+      asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(pan + 8u * (c * RS + i)));
+      D[i][c] = v.x;
+      D[i + 1][c] = v.y;
+    }
+  // rows past the panel read scratch (the allocation has 8T+32 doubles of
+  // slack) and are never stored: unconditional loads, predicated stores
 #pragma unroll
   for (int q = 0; q < R; ++q)
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (lane + 32 * q < rows) sts64(pan + 8u * (c * RS + lane + 32 * q), x[q][c]);
+    for (int c = 0; c < 8; ++c) x[q][c] = lds64(pan + 8u * (c * RS + lane + 32 * q));
+  // no early exit: a failed column only poisons columns >= it, which the
+  // failure write set never stores, and the loop stays one basic block
+  int f = 0;
+  bool special = false;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double piv = D[c][c];
+    if (f == 0 && gcol0 + c < n && piv <= 0.0) f = c + 1;
+    special |= f == 0 && rsqrt_special(piv);
+    const double inv = rsqrt_nb(piv);
+    D[c][c] = piv * inv;
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i) D[i][c] *= inv;
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[q][c] *= inv;
+#pragma unroll
+    for (int c2 = c + 1; c2 < 8; ++c2) {
+#pragma unroll
+      for (int i = c2; i < 8; ++i) D[i][c2] -= D[i][c] * D[c2][c];
+#pragma unroll
+      for (int q = 0; q < R; ++q) x[q][c2] -= x[q][c] * D[c2][c];
+    }
+  }
+  if (special) return cta_factor_panel_exact(pan, RS, rows, lane, gcol0, n);  // warp-uniform (D is redundant)
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sts64_if(pan + 8u * (c * RS + lane + 32 * q), x[q][c], lane + 32 * q < rows);
   return f;
 }
 
@@ -124,8 +168,10 @@ __device__ __forceinline__ int cta_factor_panel(uint32_t pan, int RS, int rows, 
 // then go back to shared memory.  Returns true when the panel warp reported
 // a failure (the block is then left untouched).
 template <int T, int NU, int NS>
-__device__ __forceinline__ bool cta_update_block(uint32_t sbase, int k1, int uw, int g, int t, const int* sh_fail) {
+__device__ __forceinline__ bool cta_update_block(uint32_t sbase, int k1, int uw, int g, int t, const int* sh_fail,
+                                                 uint64_t* landed) {
   constexpr int NTH = 32 * (NU + 1);
+  if (landed) mbar_wait(landed, 0);  // column block k1 staged (streamed staging)
   const int RS = cta_pstride(T, k1);
   const uint32_t pan = sbase + 8u * cta_pbase(T, k1);
   double acc[NS > 0 ? NS : 1][2];
@@ -136,20 +182,69 @@ __device__ __forceinline__ bool cta_update_block(uint32_t sbase, int k1, int uw,
     acc[s][1] = lds64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g));
   }
   uint32_t pl = sbase + 8u * (8 * k1 + g);  // row 8*k1 + g of panel 0
-  for (int l = 0; l < k1; ++l) {
-    if (l == k1 - 1) {
-      named_sync(1, NTH);  // wait for panel k1-1
-      if (*(volatile const int*)sh_fail) return true;
-    }
-    const int RL = cta_pstride(T, l);
+  constexpr int NSX = NS > 0 ? NS : 1;
+  // fragments of panel l: b = -L(8k1+g, 4kk+t), a[s] = L(8k1+8I_s+g, 4kk+t)
+  auto load = [&](uint32_t plv, int RL, double (&b)[2], double (&a)[2][NSX]) {
 #pragma unroll
     for (int kk = 0; kk < 2; ++kk) {
-      const uint32_t col = pl + 8u * ((4 * kk + t) * RL);
-      const double bneg = -lds64(col);
+      const uint32_t col = plv + 8u * ((4 * kk + t) * RL);
+      b[kk] = -lds64(col);
 #pragma unroll
-      for (int s = 0; s < NS; ++s) dmma(acc[s][0], acc[s][1], lds64(col + 8u * (8 * (uw + NU * s))), bneg);
+      for (int s = 0; s < NS; ++s) a[kk][s] = lds64(col + 8u * (8 * (uw + NU * s)));
     }
-    pl += 8u * (8 * RL - 8);
+  };
+  auto mma = [&](double (&c)[NSX][2], const double (&b)[2], const double (&a)[2][NSX]) {
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+      for (int s = 0; s < NS; ++s) dmma(c[s][0], c[s][1], a[kk][s], b[kk]);
+  };
+  int l = 0;
+  if constexpr (NS <= 4) {
+    // few tiles: two panels per trip into two accumulator sets, all fragment
+    // loads first, so neither shared-memory latency nor the DMMA chain stalls
+    double acc2[NSX][2];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc2[s][0] = acc2[s][1] = 0.0;
+    for (; l + 2 <= k1 - 1; l += 2) {
+      const int RL0 = cta_pstride(T, l), RL1 = RL0 - 8;
+      const uint32_t pl1 = pl + 8u * (8 * RL0 - 8);
+      double b0[2], a0[2][NSX], b1[2], a1[2][NSX];
+      load(pl, RL0, b0, a0);
+      load(pl1, RL1, b1, a1);
+      mma(acc, b0, a0);
+      mma(acc2, b1, a1);
+      pl = pl1 + 8u * (8 * RL1 - 8);
+    }
+    if (l < k1 - 1) {
+      const int RL = cta_pstride(T, l);
+      double b0[2], a0[2][NSX];
+      load(pl, RL, b0, a0);
+      mma(acc2, b0, a0);
+      pl += 8u * (8 * RL - 8);
+      ++l;
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      acc[s][0] += acc2[s][0];
+      acc[s][1] += acc2[s][1];
+    }
+  } else {
+    for (; l < k1 - 1; ++l) {
+      const int RL = cta_pstride(T, l);
+      double b0[2], a0[2][NSX];
+      load(pl, RL, b0, a0);
+      mma(acc, b0, a0);
+      pl += 8u * (8 * RL - 8);
+    }
+  }
+  if (uw == 0 && (threadIdx.x & 31) == 0) { PB_STAMP(40 + k1) }
+  named_sync(1, NTH);  // wait for panel k1-1
+  if (*(volatile const int*)sh_fail) return true;
+  {
+    double b0[2], a0[2][NSX];
+    load(pl, cta_pstride(T, l), b0, a0);
+    mma(acc, b0, a0);
   }
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
@@ -164,12 +259,14 @@ template <int T, int NU, int PM>
 __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_constant__ PotrfCtaArgs P) {
   constexpr int NTH = 32 * (NU + 1);
   constexpr int R = (8 * T + 31) / 32;           // rows per lane in the panel warp
-  constexpr int SLOTS = (T + NU - 1) / NU;       // tiles per update warp
+  constexpr int SLOTS = (T - 1 + NU - 1) / NU;   // tiles per update warp (blocks k1 >= 1 have <= T-1)
+  static_assert(SLOTS <= 11, "cta_update_block dispatch covers at most 11 tiles");
   extern __shared__ __align__(16) double sm[];
-  __shared__ int sh_fail;
-  __shared__ __align__(8) uint64_t sh_bar;
+  __shared__ int sh_fail, sh_rot;
+  __shared__ __align__(8) uint64_t sh_bar[T];  // one per column panel (streamed staging)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const long long p = blockIdx.x;
+  if (tid == 0) { PB_STAMP(0) }
   if (P.skip_nonzero && P.info[p] != 0) return;
   const int n = P.nvec ? P.nvec[p] : P.n;
   if (n <= 0) {
@@ -179,29 +276,47 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   double* a = P.a + (P.offs ? P.offs[p] : p * P.stride);
   const long long lda = P.nvec ? (PM ? ((n + 3) & ~3) : n) : P.lda;
   const int TT = (n + 7) >> 3;
-  const uint32_t sbase = smem_u32(sm), colb = sbase + 8u * cta_pbase(T, T);
+  const uint32_t sbase = smem_u32(sm);
 
   // ---- stage the lower triangle (panel k: rows 8k.. of columns 8k..8k+7) ----
   const double* sa = P.src ? P.src + (P.offs ? P.offs[p] : p * P.src_stride) : a;
   const long long sld = P.src ? (P.nvec ? lda : P.src_ld) : lda;
   const bool bulk = !PM && !P.upper && (sld % 2 == 0) && ((reinterpret_cast<uintptr_t>(sa) & 15) == 0) &&
                     (n % 2 == 0);
-  if (bulk) {
-    // one TMA bulk copy per column (rows 8k..n-1 of column col, k = col/8)
+  // streamed: every column panel has its own mbarrier and the factorization
+  // starts as soon as panel 0 has landed (the rest arrives underneath it).
+  // One TMA bulk copy per column (rows 8k..n-1 of column col, k = col/8);
+  // issuing from many threads at once beats one issuing lane.
+  const bool streamed = bulk && !(n & 7) && !P.pa;
+  if (streamed) {
     if (tid == 0) {
-      mbar_init(&sh_bar, 1);
+      for (int k = 0; k < TT; ++k) mbar_init(&sh_bar[k], 1);
       fence_mbar_init();
-      uint32_t bytes = 0;
-      for (int k = 0; k < TT; ++k) bytes += 8u * (uint32_t)min(8, n - 8 * k) * (uint32_t)(n - 8 * k);
-      mbar_arrive_expect_tx(&sh_bar, bytes);
+      for (int k = 0; k < TT; ++k) mbar_arrive_expect_tx(&sh_bar[k], 64u * (uint32_t)(n - 8 * k));
     }
     __syncthreads();
     for (int col = tid; col < n; col += NTH) {
       const int k = col >> 3, c = col & 7, r0 = 8 * k;
       bulk_g2s(sm + cta_pbase(T, k) + c * cta_pstride(T, k), sa + r0 + (long long)col * sld,
-               8u * (uint32_t)(n - r0), &sh_bar);
+               8u * (uint32_t)(n - r0), &sh_bar[k]);
     }
-    mbar_wait(&sh_bar, 0);
+  } else if (bulk) {
+    // one TMA bulk copy per column (rows 8k..n-1 of column col, k = col/8)
+    if (tid == 0) {
+      mbar_init(&sh_bar[0], 1);
+      fence_mbar_init();
+      uint32_t bytes = 0;
+      for (int k = 0; k < TT; ++k) bytes += 8u * (uint32_t)min(8, n - 8 * k) * (uint32_t)(n - 8 * k);
+      mbar_arrive_expect_tx(&sh_bar[0], bytes);
+    }
+    __syncthreads();
+    for (int col = tid; col < n; col += NTH) {
+      const int k = col >> 3, c = col & 7, r0 = 8 * k;
+      bulk_g2s(sm + cta_pbase(T, k) + c * cta_pstride(T, k), sa + r0 + (long long)col * sld,
+               8u * (uint32_t)(n - r0), &sh_bar[0]);
+    }
+    mbar_wait(&sh_bar[0], 0);
+  
   } else {
     const bool pairs = !PM && !P.upper && (sld % 2 == 0) && ((reinterpret_cast<uintptr_t>(sa) & 15) == 0);
     for (int k = 0; k < TT; ++k) {
@@ -226,7 +341,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       }
     }
   }
-  cp_async_wait_all();
+  if (!streamed) cp_async_wait_all();
   __syncthreads();
   if (n & 7) {  // identity padding for rows/columns past n
     for (int k = 0; k < TT; ++k) {
@@ -268,25 +383,39 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       sts64(pj + 8u * ((2 * t + 1) * RJ + rr), d1);
     }
   }
-  if (tid == 0) sh_fail = 0;
+  // Role rotation: the scheduler partition (SMSP) of a warp is its hardware
+  // slot mod 4, and consecutive CTAs get consecutive slots, so a fixed
+  // "warp 0 = panel warp" piles every panel warp of an SM onto the same
+  // partitions.  Warp 0 reads its slot and rotates the roles so the panel
+  // warps of neighbouring CTAs land on different partitions.
+  if (tid == 0) {
+    sh_fail = 0;
+    uint32_t wid;
+    asm volatile("mov.u32 %0, %%warpid;\n" : "=r"(wid));
+    sh_rot = (int)((wid >> 2) % (NU + 1));
+  }
   __syncthreads();
+  const int lw = (warp + NU + 1 - sh_rot) % (NU + 1);  // logical role: 0 = panel warp
 
   int fail = 0;
   if (P.syrk_only) {
     // no factorization: fall through to the write back of the lower triangle
-  } else if (warp == 0) {
+  } else if (lw == 0) {
     // ------------------------------------------------------------ panel warp
     for (int k = 0; k < TT; ++k) {
       if (k > 0) named_sync(2, NTH);  // block k updated and stored
+      if (lane == 0) { PB_STAMP(4 + 2 * k) }
       const int RS = cta_pstride(T, k), rows = 8 * (TT - k);
-      const int f = cta_factor_panel<R>(sbase + 8u * cta_pbase(T, k), RS, rows, lane, colb, 8 * k, n);
+      if (streamed) mbar_wait(&sh_bar[k], 0);
+      const int f = cta_factor_panel<R>(sbase + 8u * cta_pbase(T, k), RS, rows, lane, 8 * k, n);
       if (f && lane == 0) sh_fail = 8 * k + f;
+      if (lane == 0) { PB_STAMP(5 + 2 * k) }
       named_sync(1, NTH);  // panel k published (or the failure flag)
       if (f) break;
     }
   } else {
     // ------------------------------------------------------------ update warps
-    const int uw = warp - 1;
+    const int uw = lw - 1;
     for (int k1 = 1; k1 < TT; ++k1) {  // block to update; panel k1-1 is being factored
       const int ta = TT - k1;
       const int ns = uw < ta ? (ta - uw + NU - 1) / NU : 0;  // this warp's active tiles
@@ -294,9 +423,10 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       switch (ns) {  // every case fully static: no predicated tensor-core instructions
 #define PB_UPD(NSV) \
   case NSV:         \
-    if constexpr (NSV <= SLOTS) stop = cta_update_block<T, NU, NSV>(sbase, k1, uw, g, t, &sh_fail); \
+    if constexpr (NSV <= SLOTS) stop = cta_update_block<T, NU, NSV>(sbase, k1, uw, g, t, &sh_fail, streamed ? &sh_bar[k1] : nullptr); \
     break;
-        PB_UPD(0) PB_UPD(1) PB_UPD(2) PB_UPD(3) PB_UPD(4) PB_UPD(5) PB_UPD(6) PB_UPD(7)
+        PB_UPD(0) PB_UPD(1) PB_UPD(2) PB_UPD(3) PB_UPD(4) PB_UPD(5) PB_UPD(6) PB_UPD(7) PB_UPD(8) PB_UPD(9)
+        PB_UPD(10) PB_UPD(11)
 #undef PB_UPD
       }
       if (stop) {
@@ -307,8 +437,11 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
     }
     if (!fail) named_sync(1, NTH);  // the last panel's publication
   }
+  if (streamed)  // a failure can stop before late panels land: no async copy may outlive the CTA
+    for (int k = 0; k < TT; ++k) mbar_wait(&sh_bar[k], 0);
   __syncthreads();
   fail = sh_fail;
+  if (tid == 0) { PB_STAMP(2) }
 
   // ---- write back (failure: only the tiles the reference had stored) ----
   int band_lo = n, band_cols = 0;
@@ -319,6 +452,8 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   const int ncols = fail ? band_cols : n;
   const bool zf = P.zero_fill;
   if (!PM && !P.upper && !zf && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (n % 2 == 0)) {
+    // one TMA bulk store per column for the 16-byte aligned part of rows [col, rlim);
+    // an odd first row goes alone (its pair partner is in the opposite triangle)
     // one TMA bulk store per column for the 16-byte aligned part of rows [col, rlim);
     // an odd first row goes alone (its pair partner is in the opposite triangle)
     fence_proxy_async();
@@ -352,15 +487,19 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
     }
   }
   if (tid == 0) P.info[p] = fail ? fail + P.info_offset : 0;
+  if (tid == 0) { PB_STAMP(3) }
 }
 
 template <int T, int NU, int PM>
 static cudaError_t cta_launch_t(const PotrfCtaArgs& P, cudaStream_t s) {
-  const size_t smem = (size_t)(cta_pbase(T, T) + 8) * sizeof(double);
+  const size_t smem = (size_t)(cta_pbase(T, T) + 8 * T + 32) * sizeof(double);  // + panel-warp read slack
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(potrf_cta_kernel<T, NU, PM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // residency is bounded by shared memory: ask for the largest carveout
+    e = cudaFuncSetAttribute(potrf_cta_kernel<T, NU, PM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -368,12 +507,35 @@ static cudaError_t cta_launch_t(const PotrfCtaArgs& P, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// PBGPU_POTRF_NU=1|2|3 overrides the number of update warps (tuning only)
+static int nu_override() {
+  static const int v = [] {
+    const char* e = getenv("PBGPU_POTRF_NU");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// an update warp owns at most 11 tiles of a column block (cta_update_block's switch)
+template <int T, int NU>
+constexpr bool nu_ok() { return (T - 1 + NU - 1) / NU <= 11; }
+
+template <int T, int NUDEF, int PM>
+static cudaError_t launch_nu(const PotrfCtaArgs& P, cudaStream_t s) {
+  static_assert(nu_ok<T, NUDEF>(), "too many tiles per update warp");
+  const int nu = nu_override();
+  if constexpr (nu_ok<T, 1>()) if (nu == 1) return cta_launch_t<T, 1, PM>(P, s);
+  if constexpr (nu_ok<T, 2>()) if (nu == 2) return cta_launch_t<T, 2, PM>(P, s);
+  if (nu == 3) return cta_launch_t<T, 3, PM>(P, s);
+  return cta_launch_t<T, NUDEF, PM>(P, s);
+}
+
 template <int PM>
 static cudaError_t cta_dispatch(const PotrfCtaArgs& P, int nmax, cudaStream_t s) {
   switch ((nmax + 7) / 8) {
 #define PB_CASE(TV, NUV) \
   case TV:               \
-    return cta_launch_t<TV, NUV, PM>(P, s);
+    return launch_nu<TV, NUV, PM>(P, s);
     PB_CASE(1, 1) PB_CASE(2, 1) PB_CASE(3, 1) PB_CASE(4, 1) PB_CASE(5, 2) PB_CASE(6, 2)
     PB_CASE(7, 3) PB_CASE(8, 3) PB_CASE(9, 3) PB_CASE(10, 3) PB_CASE(11, 3) PB_CASE(12, 3)
     PB_CASE(13, 3) PB_CASE(14, 3) PB_CASE(15, 3) PB_CASE(16, 3) PB_CASE(17, 3) PB_CASE(18, 3)
