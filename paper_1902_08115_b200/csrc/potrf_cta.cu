@@ -536,8 +536,10 @@ static cudaError_t cta_dispatch(const PotrfCtaArgs& P, int nmax, cudaStream_t s)
 #define PB_CASE(TV, NUV) \
   case TV:               \
     return launch_nu<TV, NUV, PM>(P, s);
-    PB_CASE(1, 1) PB_CASE(2, 1) PB_CASE(3, 1) PB_CASE(4, 1) PB_CASE(5, 2) PB_CASE(6, 2)
-    PB_CASE(7, 3) PB_CASE(8, 3) PB_CASE(9, 3) PB_CASE(10, 3) PB_CASE(11, 3) PB_CASE(12, 3)
+    // update warps per order, measured (tools/quick_potrf.py, PBGPU_POTRF_NU sweeps):
+    // one update warp keeps the most CTAs resident up to n = 80
+    PB_CASE(1, 1) PB_CASE(2, 1) PB_CASE(3, 1) PB_CASE(4, 1) PB_CASE(5, 1) PB_CASE(6, 1)
+    PB_CASE(7, 1) PB_CASE(8, 1) PB_CASE(9, 1) PB_CASE(10, 1) PB_CASE(11, 2) PB_CASE(12, 2)
     PB_CASE(13, 3) PB_CASE(14, 3) PB_CASE(15, 3) PB_CASE(16, 3) PB_CASE(17, 3) PB_CASE(18, 3)
     PB_CASE(19, 3) PB_CASE(20, 3)
 #undef PB_CASE

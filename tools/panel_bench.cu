@@ -54,7 +54,7 @@ __device__ __forceinline__ int piped(uint32_t pan, int RS, int rows, int lane) {
 #pragma unroll
   for (int q = 0; q < R; ++q)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) x[q][c] = (lane + 32 * q < rows) ? lds64(pan + 8u * (c * RS + lane + 32 * q)) : 0.0;
+    for (int c = 0; c < 8; ++c) x[q][c] = lds64(pan + 8u * (c * RS + lane + 32 * q));
   int f = 0;
 #pragma unroll
   for (int c = 0; c <= 8; ++c) {
@@ -85,7 +85,7 @@ __device__ __forceinline__ int piped(uint32_t pan, int RS, int rows, int lane) {
   for (int q = 0; q < R; ++q)
 #pragma unroll
     for (int c = 0; c < 8; ++c)
-      if (lane + 32 * q < rows) sts64(pan + 8u * (c * RS + lane + 32 * q), x[q][c]);
+      sts64_if(pan + 8u * (c * RS + lane + 32 * q), x[q][c], lane + 32 * q < rows);
   return f;
 }
 
@@ -140,6 +140,42 @@ __device__ __forceinline__ int chol_then_trsm(uint32_t pan, int RS, int rows, in
   return f;
 }
 
+
+// V4: rows only, the diagonal block's column broadcast by shuffles (no redundant D)
+template <int R>
+__device__ __forceinline__ int shfl_panel(uint32_t pan, int RS, int rows, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  double x[R][8];
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[q][c] = lds64(pan + 8u * (c * RS + lane + 32 * q));
+  int f = 0;
+  bool special = false;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const double piv = __shfl_sync(FULL, x[0][c], c);
+    if (f == 0 && piv <= 0.0) f = c + 1;
+    special |= f == 0 && rsqrt_special(piv);
+    const double inv = rsqrt_nb(piv);
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[q][c] *= inv;
+    // lanes c+1..7 hold L(c2, c) in x[0][c]
+#pragma unroll
+    for (int c2 = c + 1; c2 < 8; ++c2) {
+      const double l = __shfl_sync(FULL, x[0][c], c2);
+#pragma unroll
+      for (int q = 0; q < R; ++q) x[q][c2] -= x[q][c] * l;
+    }
+  }
+  if (lane < 8) {}  // diagonal: x[0][lane] = piv * inv already (x * inv with x == piv)
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sts64_if(pan + 8u * (c * RS + lane + 32 * q), x[q][c], lane + 32 * q < rows);
+  return f + special;
+}
+
 template <int R, int V>
 __global__ void bench(long long* cyc, double* sink, int T) {
   extern __shared__ __align__(16) double sm[];
@@ -157,7 +193,7 @@ __global__ void bench(long long* cyc, double* sink, int T) {
     if (V == 0) f += chain_only(pan, RS);
     if (V == 1) f += cta_factor_panel<R>(pan, RS, rows, lane, 0, 1 << 20);
     if (V == 2) f += piped<R>(pan, RS, rows, lane);
-    if (V == 3) f += chol_then_trsm<R>(pan, RS, rows, lane);
+    if (V == 3) f += shfl_panel<R>(pan, RS, rows, lane);
   }
   long long t1 = clock64();
   if (lane == 0) cyc[blockIdx.x] = (t1 - t0) / 64;
@@ -178,7 +214,7 @@ void run(int T) {
     bench<R, 2><<<1, 32, smem>>>(c, s, T); cudaDeviceSynchronize(); r[2] = c[0];
     bench<R, 3><<<1, 32, smem>>>(c, s, T); cudaDeviceSynchronize(); r[3] = c[0];
   }
-  printf("T=%2d R=%d: chain-only %lld  current %lld  piped %lld  chol-then-trsm %lld  (%s)\n", T, R, r[0], r[1], r[2],
+  printf("T=%2d R=%d: chain-only %lld  current %lld  piped %lld  shfl %lld  (%s)\n", T, R, r[0], r[1], r[2],
          r[3], cudaGetErrorString(cudaGetLastError()));
 }
 
