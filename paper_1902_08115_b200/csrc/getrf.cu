@@ -217,6 +217,8 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
     const char* e = getenv("PBGPU_GETRF_KERNEL");
     return e && e[0] == 's';
   }();
+  if (!legacy && getrf_reg_ok(L.m, L.n))
+    return getrf_reg_launch(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, L.batch, s);
   if (fits_smem(L.m, L.n) && !legacy && L.m <= 224)
     return getrf_cta_launch(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, 0, 0, L.batch, s);
   if (fits_smem(L.m, L.n))
@@ -227,12 +229,16 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
   while (nb > 8 && !fits_smem(L.m, nb)) nb /= 2;
   if (!fits_smem(L.m, nb)) return cudaErrorInvalidValue;
   if (fits_smem(L.m, 96) && L.n <= 192) nb = 96;
+  const bool rows = !legacy && getrf_rows_ok(L.m, 64);
+  if (rows) nb = 64;  // tall panels on the row-resident kernel
   for (int j0 = 0; j0 < minmn; j0 += nb) {
     const int jb = std::min(nb, minmn - j0);
     const int mm = L.m - j0;
     double* panel = L.a + (long long)j0 + (long long)j0 * L.lda;
     // 1. factor the tall panel rows j0.., cols j0..j0+jb (pivots offset by j0)
-    cudaError_t e = (!legacy && mm <= 224)
+    cudaError_t e = rows ? getrf_rows_launch(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info, j0,
+                                             j0 > 0, L.batch, s)
+                    : (!legacy && mm <= 224)
                         ? getrf_cta_launch(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info, j0,
                                            j0 > 0, L.batch, s)
                         : getrf_smem(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info, j0,

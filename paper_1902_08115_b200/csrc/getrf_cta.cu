@@ -21,6 +21,7 @@
 // (same order, same result as factor.hpp:175-183's eager swaps).  Loads and
 // stores are per-column TMA bulk copies.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) getrf_cta_kernel(const __grid_c
   extern __shared__ __align__(16) double sm[];
   __shared__ int piv_s[2][8];
   __shared__ int piv_all[224];  // local pivot rows (0-based) of every column
-  __shared__ double scr[16];
+  __shared__ __align__(16) double scr[16];
   __shared__ int first_zero;
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -151,14 +152,23 @@ __global__ void __launch_bounds__(32 * (NU + 1)) getrf_cta_kernel(const __grid_c
   const int nblk = (minmn + 7) >> 3;
   if (warp == 0) {
     // ---------------------------------------------------------------- panel warp
+    // Rows never move inside the panel: each register slot tracks its row's
+    // current LAPACK position, a pivot step updates two positions, and the
+    // panel is written back at the final positions (the same result as the
+    // reference's sequential swaps, factor.hpp:149-156).
+    const uint32_t ubuf0 = smem_u32(&scr[0]);
     for (int k = 0; k < nblk; ++k) {
       if (k > 0) gsync(2, NTH);  // block k fully updated
-      const int c0 = 8 * k, w = min(8, minmn - c0), rows = m - c0;
+      const int c0 = 8 * k, w = min(8, minmn - c0);
       int* pv = piv_s[k & 1];
       double x[R][8];
+      int pos[R];
+      bool done[R];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         const int r = c0 + lane + 32 * q;
+        pos[q] = r;
+        done[q] = r >= m;
 #pragma unroll
         for (int c = 0; c < 8; ++c) x[q][c] = (r < m && c < w) ? sm[r + (long long)(c0 + c) * S] : 0.0;
       }
@@ -166,75 +176,56 @@ __global__ void __launch_bounds__(32 * (NU + 1)) getrf_cta_kernel(const __grid_c
       for (int c = 0; c < 8; ++c) {  // static column index: no register-array selects
         if (c >= w) break;
         const int col = c0 + c;
-        // pivot: max |v| over rows >= col, strict '>' (lowest row wins ties)
-        double bv = -1.0;
-        int bi = 0x7fffffff;
+        // pivot: max |v| (NaN never wins), ties to the lowest position, as
+        // three reductions over the non-negative doubles' bit patterns
+        unsigned long long bk = 0;
+        unsigned bp = 0xffffffffu;
+        bool dnan = false;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
-          const int r = c0 + lane + 32 * q;
           const double v = fabs(x[q][c]);
-          if (r >= col && r < m && v > bv) { bv = v; bi = r; }
+          const unsigned long long key = isnan(v) ? 0ull : (unsigned long long)__double_as_longlong(v);
+          const bool better = !done[q] && (key > bk || (key == bk && (unsigned)pos[q] < bp));
+          bk = better ? key : bk;
+          bp = better ? (unsigned)pos[q] : bp;
+          dnan |= !done[q] && pos[q] == col && isnan(v);
         }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-        }
-        // col - c0 = c < 8: the diagonal row sits in slot q = 0 of lane c
-        const double dg = __shfl_sync(0xffffffffu, x[0][c], c);
-        int pr = bi;
-        if (isnan(dg) || bi == 0x7fffffff) pr = col;
-        const int lp = (pr - c0) & 31, qp = (pr - c0) >> 5;
-        double pvl = 0.0;
+        const bool has = bp != 0xffffffffu;
+        const unsigned hi = (unsigned)(bk >> 32), lo = (unsigned)bk;
+        const unsigned khi = __reduce_max_sync(0xffffffffu, has ? hi : 0u);
+        const unsigned klo = __reduce_max_sync(0xffffffffu, has && hi == khi ? lo : 0u);
+        const unsigned q0 = __reduce_min_sync(0xffffffffu, has && hi == khi && lo == klo ? bp : 0xffffffffu);
+        const int pr = __any_sync(0xffffffffu, dnan) ? col : (int)q0;  // a NaN diagonal keeps its row
+        // pivot row (from c, pairs) to every lane through shared scratch
+        const uint32_t ub = ubuf0 + (c & 1) * 64;
 #pragma unroll
         for (int q = 0; q < R; ++q)
-          if (q == qp) pvl = x[q][c];
-        const double pivv = __shfl_sync(0xffffffffu, pvl, lp);
+          if (!done[q] && pos[q] == pr)
+#pragma unroll
+            for (int cc = c & ~1; cc < 8; cc += 2) sts128(ub + 8u * cc, x[q][cc], x[q][cc + 1]);
+        __syncwarp();
+        double u[8];
+#pragma unroll
+        for (int cc = c & ~1; cc < 8; cc += 2) lds128(ub + 8u * cc, u[cc], u[cc + 1]);
+        const bool nz = u[c] != 0.0;
         if (lane == 0) {
           pv[c] = pr;
           piv_all[col] = pr;
           ipiv[col] = pr + 1 + P.piv_offset;
+          if (!nz && first_zero == 0) first_zero = col + 1;
         }
-        const bool nz = pivv != 0.0;
-        if (nz && pr != col) {
-          // exchange panel rows col (lane c, slot 0) and pr (lane lp, slot qp)
-          if (lane == c)
-#pragma unroll
-            for (int cc = 0; cc < 8; ++cc) scr[cc] = x[0][cc];
-#pragma unroll
-          for (int q = 0; q < R; ++q)
-            if (lane == lp && q == qp)
-#pragma unroll
-              for (int cc = 0; cc < 8; ++cc) scr[8 + cc] = x[q][cc];
-          __syncwarp();
-          if (lane == c)
-#pragma unroll
-            for (int cc = 0; cc < 8; ++cc) x[0][cc] = scr[8 + cc];
-#pragma unroll
-          for (int q = 0; q < R; ++q)
-            if (lane == lp && q == qp)
-#pragma unroll
-              for (int cc = 0; cc < 8; ++cc) x[q][cc] = scr[cc];
-          __syncwarp();
-        } else if (!nz && lane == 0 && first_zero == 0) {
-          first_zero = col + 1;
-        }
-        // pivot row (after the exchange) to every lane
-        double u[8];
-#pragma unroll
-        for (int cc = c; cc < 8; ++cc) u[cc] = __shfl_sync(0xffffffffu, x[0][cc], c);
-        const double inv = nz ? 1.0 / u[c] : 0.0;
+        const double inv = nz ? __drcp_rn(u[c]) : 0.0;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
-          const int r = c0 + lane + 32 * q;
-          if (r > col && r < m) {
+          if (nz && !done[q]) pos[q] = pos[q] == pr ? col : (pos[q] == col ? pr : pos[q]);
+          const bool act = !done[q] && pos[q] != col;
+          done[q] = done[q] || pos[q] == col;
+          if (act) {
             if (nz) x[q][c] *= inv;
             const double f = x[q][c];
             if (f != 0.0)
 #pragma unroll
-              for (int c2 = c + 1; c2 < 8; ++c2)
-                if (c2 < w) x[q][c2] -= f * u[c2];
+              for (int c2 = c + 1; c2 < 8; ++c2) x[q][c2] = fma(-f, u[c2], x[q][c2]);
           }
         }
       }
@@ -244,7 +235,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) getrf_cta_kernel(const __grid_c
         if (r < m)
 #pragma unroll
           for (int c = 0; c < 8; ++c)
-            if (c < w) sm[r + (long long)(c0 + c) * S] = x[q][c];
+            if (c < w) sm[pos[q] + (long long)(c0 + c) * S] = x[q][c];
       }
       gsync(1, NTH);  // panel k (+ its pivots) published
     }
@@ -325,13 +316,20 @@ cudaError_t getrf_cta_launch(double* a, long long stride, int lda, int m, int n,
   if (S < m8) S += 16;
   P.S = S;
   if ((size_t)S * ((n + 7) & ~7) * sizeof(double) > 220 * 1024) return cudaErrorInvalidValue;
-  // update warps sized to the work: one for n <= 40, two up to 96, three above
-  const int nu = n <= 40 ? 1 : (n <= 96 ? 2 : 3);
+  // update warps sized to the work (measured, tools/sweep_getrf_nu.sh): one up
+  // to n = 48, three above (PBGPU_GETRF_NU = 1|2|3|5|7 overrides, tuning only)
+  static const int nu_env = [] {
+    const char* e = getenv("PBGPU_GETRF_NU");
+    return e ? atoi(e) : 0;
+  }();
+  const int nu = nu_env ? nu_env : (n <= 48 ? 1 : 3);
   switch ((m + 31) / 32) {
 #define PB_R(RV)                                      \
   case RV:                                            \
     if (nu == 1) return getrf_cta_t<RV, 1>(P, batch, s); \
     if (nu == 2) return getrf_cta_t<RV, 2>(P, batch, s); \
+    if (nu == 5) return getrf_cta_t<RV, 5>(P, batch, s); \
+    if (nu == 7) return getrf_cta_t<RV, 7>(P, batch, s); \
     return getrf_cta_t<RV, 3>(P, batch, s);
     PB_R(1) PB_R(2) PB_R(3) PB_R(4) PB_R(5) PB_R(6) PB_R(7)
 #undef PB_R

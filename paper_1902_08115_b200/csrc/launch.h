@@ -79,6 +79,11 @@ cudaError_t potrf_warp_launch(double* a, long long stride, int lda, int n, int u
 cudaError_t potrf_cta_launch(double* a, long long stride, const long long* offs, const int* nvec, int lda,
                              int n, int upper, int pm, int zero_fill, int* info, int info_offset,
                              int skip_nonzero, int batch, cudaStream_t s);
+// register-resident segment-per-problem Cholesky, n <= 32 (potrf_reg.cu); same
+// contract as potrf_cta_launch, which forwards orders <= 32 here
+cudaError_t potrf_reg_launch(double* a, long long stride, const long long* offs, const int* nvec, int lda, int nmax,
+                             int upper, int pm, int zero_fill, int* info, int info_offset, int skip_nonzero,
+                             int batch, cudaStream_t s);
 // same kernel with the prologue S = C + A B^T (A, B n x k, same storage kind as C)
 // (D may differ from C: the kernel stages from c and writes d)
 cudaError_t syrk_potrf_cta_launch(double* d, long long stride_d, const long long* offs, const int* nvec, int ldd,
@@ -108,6 +113,17 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s);
 // pipelined CTA-per-problem LU for shared-memory-resident problems (getrf_cta.cu)
 cudaError_t getrf_cta_launch(double* a, long long stride, int lda, int m, int n, int* ipiv, long long sp,
                              int* info, int piv_offset, int keep_info, int batch, cudaStream_t s);
+
+// register-resident warp-per-problem LU, m, n <= 32 (getrf_reg.cu)
+bool getrf_reg_ok(int m, int n);
+cudaError_t getrf_reg_launch(double* a, long long stride, int lda, int m, int n, int* ipiv, long long sp, int* info,
+                             int batch, cudaStream_t s);
+
+// row-resident CTA-per-problem LU, m <= 224 and n <= 64 (n <= 96 for m <= 96)
+// (getrf_rows.cu); piv_offset / keep_info serve the tall panels of the blocked path
+bool getrf_rows_ok(int m, int n);
+cudaError_t getrf_rows_launch(double* a, long long stride, int lda, int m, int n, int* ipiv, long long sp, int* info,
+                              int piv_offset, int keep_info, int batch, cudaStream_t s);
 
 // Triangular solve.  Column-major dtrsm (in place on b) or the panel-major
 // trsm_rltn_nd (b -> d, d may alias b).  The effective problem is always a

@@ -22,13 +22,19 @@
 // < 4*floor(p/4); test_factor.cpp:251-277).  PM = 1 addresses panel-major
 // storage (ps = 4); zero_fill writes the LowerZero band zeros of
 // syrk_potrf_nd (micro_kernel.hpp:657-673).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "launch.h"
 
 namespace pbg {
+
+constexpr int kCtaMaxT = 20;  // n <= 160
 
 struct PotrfCtaArgs {
   double* a;
@@ -53,6 +59,13 @@ struct PotrfCtaArgs {
   long long src_stride;
   int src_ld;
   int syrk_only;  // write S = C + A B^T (lower) back and skip the factorization
+  // optional per-panel TMA tensor maps (packed column-major lower problems):
+  // map k covers rows 8k .. 8k+8(T-k)+3 of columns 8k..8k+7, i.e. exactly the
+  // shared-memory panel k (column stride 8(T-k)+4, the 4 rows past n are
+  // zero-filled out of bounds), so staging and the write back are one tensor
+  // copy per panel
+  int tma;
+  CUtensorMap tm[kCtaMaxT];
 };
 
 __host__ __device__ constexpr int cta_pstride(int T, int k) { return 8 * (T - k) + 4; }
@@ -132,15 +145,13 @@ __device__ __forceinline__ int cta_factor_panel(uint32_t pan, int RS, int rows, 
   for (int q = 0; q < R; ++q)
 #pragma unroll
     for (int c = 0; c < 8; ++c) x[q][c] = lds64(pan + 8u * (c * RS + lane + 32 * q));
-  // no early exit: a failed column only poisons columns >= it, which the
-  // failure write set never stores, and the loop stays one basic block
-  int f = 0;
-  bool special = false;
+  // no failure test inside the loop: a pivot <= 0 (NaN after rsqrt_nb), a
+  // denormal or +inf pivot (rsqrt_nb inexact) and a NaN input all leave a
+  // non-finite diagonal entry, which the sum below catches; those rare
+  // panels are redone exactly (failure column, reference semantics)
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const double piv = D[c][c];
-    if (f == 0 && gcol0 + c < n && piv <= 0.0) f = c + 1;
-    special |= f == 0 && rsqrt_special(piv);
     const double inv = rsqrt_nb(piv);
     D[c][c] = piv * inv;
 #pragma unroll
@@ -155,12 +166,18 @@ __device__ __forceinline__ int cta_factor_panel(uint32_t pan, int RS, int rows, 
       for (int q = 0; q < R; ++q) x[q][c2] -= x[q][c] * D[c2][c];
     }
   }
-  if (special) return cta_factor_panel_exact(pan, RS, rows, lane, gcol0, n);  // warp-uniform (D is redundant)
+  double dsum = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) dsum += D[c][c];
+  if (!(dsum <= 1.7976931348623157e308))  // warp-uniform (D is redundant)
+    return cta_factor_panel_exact(pan, RS, rows, lane, gcol0, n);
+  // the strict upper part of the diagonal block keeps its staged (original) values
 #pragma unroll
   for (int q = 0; q < R; ++q)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) sts64_if(pan + 8u * (c * RS + lane + 32 * q), x[q][c], lane + 32 * q < rows);
-  return f;
+    for (int c = 0; c < 8; ++c)
+      sts64_if(pan + 8u * (c * RS + lane + 32 * q), x[q][c], lane + 32 * q < rows && (q > 0 || lane >= c));
+  return 0;
 }
 
 // Update warp: column block k1's tiles I = uw + NU*s (s < NS) accumulate
@@ -249,8 +266,9 @@ __device__ __forceinline__ bool cta_update_block(uint32_t sbase, int k1, int uw,
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
     const int I = uw + NU * s;
-    sts64(pan + 8u * ((2 * t) * RS + 8 * I + g), acc[s][0]);
-    sts64(pan + 8u * ((2 * t + 1) * RS + 8 * I + g), acc[s][1]);
+    // tile 0 is the diagonal block: its strict upper part is never written
+    sts64_if(pan + 8u * ((2 * t) * RS + 8 * I + g), acc[s][0], I > 0 || g >= 2 * t);
+    sts64_if(pan + 8u * ((2 * t + 1) * RS + 8 * I + g), acc[s][1], I > 0 || g >= 2 * t + 1);
   }
   return false;
 }
@@ -261,7 +279,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   constexpr int R = (8 * T + 31) / 32;           // rows per lane in the panel warp
   constexpr int SLOTS = (T - 1 + NU - 1) / NU;   // tiles per update warp (blocks k1 >= 1 have <= T-1)
   static_assert(SLOTS <= 11, "cta_update_block dispatch covers at most 11 tiles");
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(1024) double sm[];
   __shared__ int sh_fail, sh_rot;
   __shared__ __align__(8) uint64_t sh_bar[T];  // one per column panel (streamed staging)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -288,7 +306,23 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   // One TMA bulk copy per column (rows 8k..n-1 of column col, k = col/8);
   // issuing from many threads at once beats one issuing lane.
   const bool streamed = bulk && !(n & 7) && !P.pa;
-  if (streamed) {
+  if (P.tma) {
+    // one tensor copy per column panel, each on its own mbarrier
+    if (tid == 0) {
+      for (int k = 0; k < TT; ++k) mbar_init(&sh_bar[k], 1);
+      fence_mbar_init();
+      for (int k = 0; k < TT; ++k) {
+        mbar_arrive_expect_tx(&sh_bar[k], 64u * (uint32_t)cta_pstride(T, k));
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(sbase + 8u * cta_pbase(T, k)),
+            "l"(reinterpret_cast<uint64_t>(&P.tm[k])), "r"(8 * k), "r"(8 * k), "r"((int)p),
+            "r"(smem_u32(&sh_bar[k]))
+            : "memory");
+      }
+    }
+    __syncthreads();
+  } else if (streamed) {
     if (tid == 0) {
       for (int k = 0; k < TT; ++k) mbar_init(&sh_bar[k], 1);
       fence_mbar_init();
@@ -341,7 +375,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       }
     }
   }
-  if (!streamed) cp_async_wait_all();
+  if (!streamed && !P.tma) cp_async_wait_all();
   __syncthreads();
   if (n & 7) {  // identity padding for rows/columns past n
     for (int k = 0; k < TT; ++k) {
@@ -406,7 +440,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       if (k > 0) named_sync(2, NTH);  // block k updated and stored
       if (lane == 0) { PB_STAMP(4 + 2 * k) }
       const int RS = cta_pstride(T, k), rows = 8 * (TT - k);
-      if (streamed) mbar_wait(&sh_bar[k], 0);
+      if (streamed || P.tma) mbar_wait(&sh_bar[k], 0);
       const int f = cta_factor_panel<R>(sbase + 8u * cta_pbase(T, k), RS, rows, lane, 8 * k, n);
       if (f && lane == 0) sh_fail = 8 * k + f;
       if (lane == 0) { PB_STAMP(5 + 2 * k) }
@@ -423,7 +457,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       switch (ns) {  // every case fully static: no predicated tensor-core instructions
 #define PB_UPD(NSV) \
   case NSV:         \
-    if constexpr (NSV <= SLOTS) stop = cta_update_block<T, NU, NSV>(sbase, k1, uw, g, t, &sh_fail, streamed ? &sh_bar[k1] : nullptr); \
+    if constexpr (NSV <= SLOTS) stop = cta_update_block<T, NU, NSV>(sbase, k1, uw, g, t, &sh_fail, (streamed || P.tma) ? &sh_bar[k1] : nullptr); \
     break;
         PB_UPD(0) PB_UPD(1) PB_UPD(2) PB_UPD(3) PB_UPD(4) PB_UPD(5) PB_UPD(6) PB_UPD(7) PB_UPD(8) PB_UPD(9)
         PB_UPD(10) PB_UPD(11)
@@ -437,7 +471,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
     }
     if (!fail) named_sync(1, NTH);  // the last panel's publication
   }
-  if (streamed)  // a failure can stop before late panels land: no async copy may outlive the CTA
+  if (streamed || P.tma)  // a failure can stop before late panels land: no async copy may outlive the CTA
     for (int k = 0; k < TT; ++k) mbar_wait(&sh_bar[k], 0);
   __syncthreads();
   fail = sh_fail;
@@ -451,7 +485,21 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   }
   const int ncols = fail ? band_cols : n;
   const bool zf = P.zero_fill;
-  if (!PM && !P.upper && !zf && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (n % 2 == 0)) {
+  if (P.tma && !fail) {
+    // one tensor store per panel; rows past n are out of bounds (not written),
+    // the diagonal blocks' strict upper parts still hold the staged originals
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      for (int k = 0; k < TT; ++k)
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                         reinterpret_cast<uint64_t>(&P.tm[k])),
+                     "r"(8 * k), "r"(8 * k), "r"((int)p), "r"(sbase + 8u * cta_pbase(T, k))
+                     : "memory");
+      bulk_commit();
+      bulk_wait_read0();
+    }
+  } else if (!PM && !P.upper && !zf && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (n % 2 == 0)) {
     // one TMA bulk store per column for the 16-byte aligned part of rows [col, rlim);
     // an odd first row goes alone (its pair partner is in the opposite triangle)
     // one TMA bulk store per column for the 16-byte aligned part of rows [col, rlim);
@@ -547,11 +595,77 @@ static cudaError_t cta_dispatch(const PotrfCtaArgs& P, int nmax, cudaStream_t s)
   return cudaErrorInvalidValue;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 cta_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+// Per-panel tensor maps for packed lower column-major batches (the config-3
+// shape); false when the layout rules TMA out.  The last encoded set is cached
+// (the maps only depend on the base pointer and the shape).
+static bool cta_tensor_maps(PotrfCtaArgs& P) {
+  if (P.upper || P.offs || P.nvec || P.pa || P.src || P.syrk_only || P.zero_fill) return false;
+  if ((P.n & 7) || P.n <= 0 || P.n > 8 * kCtaMaxT || P.batch <= 0) return false;
+  if ((reinterpret_cast<uintptr_t>(P.a) & 15) || (P.lda & 1) || (P.batch > 1 && (P.stride & 1))) return false;
+  if (P.lda < P.n || (P.batch > 1 && P.stride < (long long)P.lda * P.n)) return false;
+  static const bool off = [] {
+    const char* e = getenv("PBGPU_POTRF_TMA");
+    return e && e[0] == '0';
+  }();
+  if (off) return false;
+  auto enc = cta_encode_fn();
+  if (!enc) return false;
+  struct Key {
+    const double* a;
+    long long stride;
+    int lda, n, batch;
+  };
+  static thread_local Key last{nullptr, 0, 0, 0, 0};
+  static thread_local CUtensorMap cache[kCtaMaxT];
+  const int T = P.n / 8;
+  if (!(last.a == P.a && last.stride == P.stride && last.lda == P.lda && last.n == P.n && last.batch == P.batch)) {
+    for (int k = 0; k < T; ++k) {
+      cuuint64_t dims[3] = {(cuuint64_t)P.n, (cuuint64_t)P.n, (cuuint64_t)P.batch};
+      cuuint64_t strides[2] = {(cuuint64_t)P.lda * 8, (cuuint64_t)(P.batch > 1 ? P.stride : (long long)P.lda * P.n) * 8};
+      cuuint32_t box[3] = {(cuuint32_t)cta_pstride(T, k), 8u, 1u};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (enc(&cache[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, P.a, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        last = Key{nullptr, 0, 0, 0, 0};
+        return false;
+      }
+    }
+    last = Key{P.a, P.stride, P.lda, P.n, P.batch};
+  }
+  for (int k = 0; k < T; ++k) P.tm[k] = cache[k];
+  return true;
+}
+
 cudaError_t potrf_cta_launch(double* a, long long stride, const long long* offs, const int* nvec, int lda,
                              int n, int upper, int pm, int zero_fill, int* info, int info_offset,
                              int skip_nonzero, int batch, cudaStream_t s) {
+  // orders <= 32: the register-resident segment kernel (potrf_reg.cu);
+  // PBGPU_POTRF_REG=0 keeps this kernel (A/B measurements)
+  static const bool reg = [] {
+    const char* e = getenv("PBGPU_POTRF_REG");
+    return !(e && e[0] == '0');
+  }();
+  if (reg && n <= 32)
+    return potrf_reg_launch(a, stride, offs, nvec, lda, n, upper, pm, zero_fill, info, info_offset, skip_nonzero,
+                            batch, s);
   PotrfCtaArgs P{a, stride, offs, nvec, lda, n, upper, batch, zero_fill, info, info_offset, skip_nonzero,
                  nullptr, nullptr, 0, nullptr, 0, 0, nullptr, 0, 0, 0};
+  P.tma = !pm && cta_tensor_maps(P);
   return pm ? cta_dispatch<1>(P, n, s) : cta_dispatch<0>(P, n, s);
 }
 

@@ -1,0 +1,147 @@
+// Register-resident batched Cholesky for small orders, n <= 32 (sm_100a).
+//
+// The small-n branch of the size switch (the paper's small-size algorithm
+// family; the reference's potrf_core, factor.hpp:45-99, with its edge
+// kernels edge_potrf / edge_trsm_right, micro_kernel.hpp:309-356).  A
+// segment of W = 8, 16 or 32 lanes owns one problem (4, 2 or 1 problems per
+// warp): lane i holds row i of the lower triangle in registers (N doubles),
+// loaded column by column so every column is one coalesced access.  The
+// factorization is right-looking over columns c:
+//   * each lane publishes its current a(i, c) to a per-warp shared column
+//     buffer (double-buffered by column parity: no write-after-read hazard);
+//   * every lane reads the pivot and the column below it back as broadcast
+//     loads, forms inv = rsqrt(pivot) (failure test `piv <= 0.0`,
+//     micro_kernel.hpp:314), scales its own entry, and applies the rank-1
+//     update a(i, c2) -= l(i, c) * a(c2, c) * inv to the columns right of c.
+// No shuffles, no barriers beyond __syncwarp, no shared-memory copy of the
+// matrix: occupancy is bounded by registers only.  Rows past n are identity
+// padding.  On a failure at column p only the reference's write set is
+// stored (rows < 8*floor((p-1)/8) + 8 of columns < 4*floor((p-1)/4); see
+// potrf_cta.cu and test_factor.cpp:251-277): those entries are final when
+// column p-1 fails, everything right of it is never written.
+#include <cstdint>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace pbg {
+
+struct PotrfRegArgs {
+  double* a;
+  long long stride;
+  const long long* offs;  // optional per-problem element offsets (variable batches)
+  const int* nvec;        // optional per-problem order (variable batches)
+  int lda, n, upper, batch, zero_fill;
+  int* info;
+  int info_offset;
+  int skip_nonzero;
+};
+
+constexpr int kRegWarps = 4;
+
+// CS != 0: compile-time column stride (packed column-major lower problems,
+// lda == n == N): every access is the row pointer plus an immediate offset.
+template <int N, int W, int PM, int CS>
+__global__ void __launch_bounds__(32 * kRegWarps, 4) potrf_reg_kernel(const __grid_constant__ PotrfRegArgs P) {
+  static_assert(N <= W && W <= 32 && 32 % W == 0, "segment shape");
+  constexpr int SEGS = 32 / W;
+  __shared__ __align__(16) double colbuf[kRegWarps][2][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = lane % W, sbase = lane - i;  // row, first lane of the segment
+  const long long p = ((long long)blockIdx.x * kRegWarps + warp) * SEGS + lane / W;
+  const bool live = p < P.batch && !(P.skip_nonzero && P.info[p] != 0);
+  const int n = live ? (P.nvec ? P.nvec[p] : P.n) : 0;
+  double* a = P.a + (live ? (P.offs ? P.offs[p] : p * P.stride) : 0);
+  const long long lda = CS ? CS : (P.nvec ? (PM ? ((n + 3) & ~3) : n) : P.lda);
+
+  // element (i, j) of the lower problem is rp[j * cs] in all three storage kinds
+  double* rp = a + (PM ? (long long)(i >> 2) * 4 * lda + (i & 3) : ((!CS && P.upper) ? (long long)i * lda : i));
+  const long long cs = CS ? CS : (PM ? 4 : (P.upper ? 1 : lda));
+  double x[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) x[j] = ldg_if(rp + j * cs, j <= i && i < n, i == j ? 1.0 : 0.0);
+
+  const uint32_t buf0 = smem_u32(&colbuf[warp][0][sbase]);
+  unsigned bad = 0;  // bit c: column c's pivot failed the test
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    const uint32_t buf = buf0 + (c & 1) * 32 * 8;
+    sts64(buf + 8u * i, x[c]);
+    __syncwarp();
+    double col[N];
+#pragma unroll
+    for (int c2 = c & ~1; c2 < N; c2 += 2) lds128(buf + 8u * c2, col[c2], col[c2 + 1]);
+    const double piv = col[c];  // == x[c] on lane c
+    bad |= (piv <= 0.0 ? 1u : 0u) << c;
+    double inv = rsqrt_nb(piv);
+    if (__any_sync(0xffffffffu, rsqrt_special(piv)))  // denormal / +inf pivots: exact path
+      inv = rsqrt_special(piv) ? rsqrt(piv) : inv;
+    x[c] *= inv;
+    const double t = x[c] * inv;
+#pragma unroll
+    for (int c2 = c + 1; c2 < N; ++c2) x[c2] = fma(-t, col[c2], x[c2]);
+  }
+  const unsigned nmask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
+  const int fail = __ffs(bad & nmask);  // first failing column, 1-based (0: none)
+
+  // ---- write back: the reference's write set, coalesced column by column ----
+  if (n > 0) {
+    int band_lo = n, ncols = n;
+    if (fail) {
+      band_lo = ((fail - 1) / 8) * 8 + 8;
+      ncols = ((fail - 1) / 4) * 4;
+    }
+    const bool row_ok = i < n && i < band_lo;
+    if (CS) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) stg_if(rp + j * CS, x[j], row_ok && j <= i && j < ncols);
+    } else {
+      double* wp = rp;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const bool lower = j <= i;
+        const bool zero = P.zero_fill && i < j && (i >> 3) == (j >> 3);
+        stg_if(wp, lower ? x[j] : 0.0, row_ok && j < ncols && (lower || zero));
+        wp += cs;
+      }
+    }
+    if (i == 0) P.info[p] = fail ? fail + P.info_offset : 0;
+  } else if (live && i == 0) {
+    P.info[p] = 0;
+  }
+}
+
+template <int N, int W, int PM>
+static cudaError_t reg_launch_t(const PotrfRegArgs& P, cudaStream_t s) {
+  constexpr int per_cta = kRegWarps * (32 / W);
+  const unsigned grid = (unsigned)((P.batch + per_cta - 1) / per_cta);
+  if constexpr (!PM) {
+    if (!P.upper && !P.nvec && !P.offs && !P.zero_fill && P.n == N && P.lda == N) {
+      potrf_reg_kernel<N, W, 0, N><<<grid, 32 * kRegWarps, 0, s>>>(P);
+      return cudaGetLastError();
+    }
+  }
+  potrf_reg_kernel<N, W, PM, 0><<<grid, 32 * kRegWarps, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
+template <int PM>
+static cudaError_t reg_dispatch(const PotrfRegArgs& P, int nmax, cudaStream_t s) {
+  if (nmax <= 4) return reg_launch_t<4, 8, PM>(P, s);
+  if (nmax <= 8) return reg_launch_t<8, 8, PM>(P, s);
+  if (nmax <= 12) return reg_launch_t<12, 16, PM>(P, s);
+  if (nmax <= 16) return reg_launch_t<16, 16, PM>(P, s);
+  if (nmax <= 24) return reg_launch_t<24, 32, PM>(P, s);
+  if (nmax <= 32) return reg_launch_t<32, 32, PM>(P, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t potrf_reg_launch(double* a, long long stride, const long long* offs, const int* nvec, int lda, int nmax,
+                             int upper, int pm, int zero_fill, int* info, int info_offset, int skip_nonzero,
+                             int batch, cudaStream_t s) {
+  if (batch <= 0) return cudaSuccess;
+  PotrfRegArgs P{a, stride, offs, nvec, lda, nmax, upper, batch, zero_fill, info, info_offset, skip_nonzero};
+  return pm ? reg_dispatch<1>(P, nmax, s) : reg_dispatch<0>(P, nmax, s);
+}
+
+}  // namespace pbg
