@@ -143,11 +143,13 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       big[nv[p]].push_back(p);
     }
   }
-  // device scratch: index lists, subset offsets/orders, subset info
+  // Small orders: sorted by order and launched per 8-column class, so every
+  // launch is sized (shared memory, warps, unrolling) for its own problems.
+  std::sort(small.begin(), small.end(), [&](int x, int y) { return nv[x] < nv[y]; });
   const size_t nsm = small.size();
-  int *d_idx = nullptr, *d_n = nullptr, *d_info = nullptr;
-  long long* d_off = nullptr;
   if (nsm) {
+    int *d_idx = nullptr, *d_n = nullptr, *d_info = nullptr;
+    long long* d_off = nullptr;
     std::vector<long long> so(nsm);
     std::vector<int> sn(nsm);
     for (size_t q = 0; q < nsm; ++q) {
@@ -161,30 +163,37 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
     cudaMemcpyAsync(d_idx, small.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_n, sn.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_off, so.data(), sizeof(long long) * nsm, cudaMemcpyHostToDevice, s);
-    const int bs = (int)nsm;
-    if (!L.pm) {
-      e = syrk_lower_cta_launch(L.C, d_off, d_n, L.A, nsmall_max, 0, d_info, bs, s);
-      if (e == cudaSuccess)
-        e = potrf_cta_launch(L.C, 0, d_off, d_n, 0, nsmall_max, 0, 0, 0, d_info, 0, 0, bs, s);
-    } else {
-      e = syrk_potrf_cta_launch(L.C, 0, d_off, d_n, 0, L.C, 0, 0, L.A, L.A, 0, 1, 0, nsmall_max, 1, 1, d_info,
-                                bs, s);
+    for (size_t b0 = 0; b0 < nsm && e == cudaSuccess;) {
+      const int cls = (sn[b0] + 7) / 8;
+      size_t b1 = b0;
+      while (b1 < nsm && (sn[b1] + 7) / 8 == cls) ++b1;
+      const int bs = (int)(b1 - b0), nmax = sn[b1 - 1];
+      int* bn = d_n + b0;
+      int* binfo = d_info + b0;
+      long long* boff = d_off + b0;
+      if (!L.pm) {
+        e = syrk_lower_cta_launch(L.C, boff, bn, L.A, nmax, 0, binfo, bs, s);
+        if (e == cudaSuccess) e = potrf_cta_launch(L.C, 0, boff, bn, 0, nmax, 0, 0, 0, binfo, 0, 0, bs, s);
+      } else {
+        e = syrk_potrf_cta_launch(L.C, 0, boff, bn, 0, L.C, 0, 0, L.A, L.A, 0, 1, 0, nmax, 1, 1, binfo, bs, s);
+      }
+      if (e == cudaSuccess) {
+        TrsmLaunch T;
+        T.pm = L.pm;
+        T.lower = 1; T.trans = 1; T.unit = 0;
+        T.mm = T.nn = nmax;
+        T.alpha = 1.0;
+        T.a = L.C; T.b = L.B; T.d = L.B;
+        T.nvec = bn; T.offs = boff;
+        T.info = binfo;
+        T.skip_nonzero = 1;
+        T.batch = bs;
+        e = trsm_launch(T, s);
+      }
+      b0 = b1;
     }
     if (e == cudaSuccess) {
-      TrsmLaunch T;
-      T.pm = L.pm;
-      T.lower = 1; T.trans = 1; T.unit = 0;
-      T.mm = T.nn = nsmall_max;
-      T.alpha = 1.0;
-      T.a = L.C; T.b = L.B; T.d = L.B;
-      T.nvec = d_n; T.offs = d_off;
-      T.info = d_info;
-      T.skip_nonzero = 1;
-      T.batch = bs;
-      e = trsm_launch(T, s);
-    }
-    if (e == cudaSuccess) {
-      scatter_info_kernel<<<std::max(1, (bs + 255) / 256), 256, 0, s>>>(d_info, d_idx, L.info, bs);
+      scatter_info_kernel<<<std::max(1, (int)((nsm + 255) / 256)), 256, 0, s>>>(d_info, d_idx, L.info, (int)nsm);
       e = cudaGetLastError();
     }
     cudaFreeAsync(d_idx, s);

@@ -17,6 +17,7 @@
 // Exactly-zero non-unit diagonals are detected before anything is written
 // (level3.hpp:292-299) and reported per problem.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -180,6 +181,11 @@ __global__ void __launch_bounds__(256) trsm_kernel(const __grid_constant__ TrsmA
 
 cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.mm <= 0 || L.nn <= 0) return cudaSuccess;
+  static const bool rlt = [] {  // PBGPU_TRSM_RLT=0 keeps this kernel for every flag set (A/B)
+    const char* e = getenv("PBGPU_TRSM_RLT");
+    return !(e && e[0] == '0');
+  }();
+  if (rlt && trsm_rlt_ok(L)) return trsm_rlt_launch(L, s);
   TrsmArgs T;
   T.L = L;
   T.rowblocks = (L.mm + TR_R - 1) / TR_R;

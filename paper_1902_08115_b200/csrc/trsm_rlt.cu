@@ -1,0 +1,215 @@
+// Batched right-side triangular solve X * A^T = alpha * B with A lower
+// ("rltn"/"rltu": the config-5 step, trsm_rltn_nd and the blocked Cholesky's
+// panel solve), warp-per-8-rows, left-looking on FP64 tensor cores (sm_100a).
+//
+// Replaces trsm_right_core / kernel_trsm_right (level3.hpp:174-214,
+// micro_kernel.hpp:522-543) and trsm_rltn_nd (level3.hpp:484-526) for this
+// flag set.  Rows of X are independent, so one warp owns 8 rows of one
+// problem and needs no barrier at all.  For column tile J (8 columns, in
+// dependency order: A^T is upper, so ascending):
+//   1. C = alpha * B(rows, J) - X(rows, 0:8J) * A(J, 0:8J)^T, accumulated with
+//      DMMA m8n8k4 in registers: the solved X lives in the warp's shared
+//      memory slice already in A-fragment order (one conflict-free 256-byte
+//      load per DMMA), the A(J, :) fragments come through L1;
+//   2. the 8x8 diagonal block is solved by substitution inside each quad of
+//      lanes (a lane owns two columns of a row; the solved value travels by
+//      shuffle), with the reference's reciprocal multiply
+//      (micro_kernel.hpp:351-352);
+//   3. the tile is stored and re-laid as A fragments for the next tiles.
+// An exactly-zero non-unit diagonal is found before any store and reported
+// (level3.hpp:292-299).  Column- and panel-major (ps = 4) storage; uniform or
+// variable (config-5) batches.
+#include <cstdint>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace pbg {
+
+constexpr int kRltWarps = 4;
+
+struct RltArgs {
+  TrsmLaunch L;
+  int rbmax;  // row blocks (8 rows) per problem slot in the grid
+  int ntmax;  // column tiles of the largest problem (shared-memory slice)
+};
+
+template <int PM>
+__device__ __forceinline__ long long rlt_off(long long ld, int r, int c) {
+  if (PM) return (long long)(r >> 2) * 4 * ld + (long long)c * 4 + (r & 3);
+  return (long long)r + (long long)c * ld;
+}
+
+// Staged rows of A: column c of the 8-row block at c*8, rows XOR-swizzled so
+// a B-fragment load (rows g, columns 4K + t) touches 16 distinct banks per
+// half-warp.
+__device__ __forceinline__ int ab_idx(int c, int g) { return c * 8 + (g ^ (((c >> 1) & 1) << 2)); }
+
+template <int PM>
+__global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_constant__ RltArgs R) {
+  extern __shared__ __align__(16) double sm_all[];
+  const TrsmLaunch& L = R.L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, tid = threadIdx.x;
+  const int cpp = (R.rbmax + kRltWarps - 1) / kRltWarps;  // CTAs per problem
+  const long long p = blockIdx.x / cpp;
+  const int rb = (int)(blockIdx.x - p * cpp) * kRltWarps + warp;
+  if (p >= L.batch) return;                              // CTA-uniform
+  if (L.skip_nonzero && L.info[p] != 0) return;          // CTA-uniform
+  int n = L.nn, m = L.mm;
+  long long lda = L.lda, ldb = L.ldb, ldd = L.ldd;
+  const double *A, *B;
+  double* D;
+  if (L.nvec) {
+    n = m = L.nvec[p];
+    lda = ldb = ldd = PM ? ((n + 3) & ~3) : n;
+    A = L.a + L.offs[p];
+    B = L.b + L.offs[p];
+    D = L.d + L.offs[p];
+  } else {
+    A = L.a + p * L.sa;
+    B = L.b + p * L.sb;
+    D = L.d + p * L.sd;
+  }
+  if ((rb - warp) * 8 >= m) return;  // CTA-uniform: no row of this CTA exists
+  // ---- zero diagonal: smallest exactly-zero index, before any store ----
+  if (!L.unit) {
+    unsigned z = 0xffffffffu;
+    for (int i = lane; i < n; i += 32)
+      if (A[rlt_off<PM>(lda, i, i)] == 0.0) z = min(z, (unsigned)i);
+    z = __reduce_min_sync(0xffffffffu, z);
+    if (z != 0xffffffffu) {  // same verdict in every warp: the CTA leaves together
+      if (rb == 0 && lane == 0 && L.info && !L.skip_nonzero) L.info[p] = (int)z + 1;
+      return;
+    }
+  }
+  const int nt = (n + 7) >> 3;
+  const int r = rb * 8 + g;
+  const bool rok = r < m;
+  const uint32_t xs = smem_u32(sm_all + (size_t)warp * R.ntmax * 64);  // [tile][kk][lane]
+  double* ab_base = sm_all + (size_t)kRltWarps * R.ntmax * 64;          // 2 x [8 * ntmax * 8]
+  const int abs = R.ntmax * 64;
+  const double alpha = L.alpha;
+  // stage rows 8J..8J+7, columns 0..8J+7 of A (16-byte pairs of rows; rows past n are zero)
+  auto stage = [&](int J) {
+    double* ab = ab_base + (J & 1) * abs;
+    const int cols = 8 * J + 8, tot = cols * 4;
+    for (int e = tid; e < tot; e += 32 * kRltWarps) {
+      const int c = e >> 2, g2 = (e & 3) * 2, row = 8 * J + g2;
+      double* dst = ab + ab_idx(c, g2);
+      const bool v0 = row < n && c < n, v1 = row + 1 < n && c < n;
+      const double* src = A + rlt_off<PM>(lda, v0 ? row : 0, v0 ? c : 0);
+      if (v1 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        cp_async16(dst, src);
+      } else {
+        cp_async8(dst, src, v0);
+        cp_async8(dst + 1, v1 ? A + rlt_off<PM>(lda, row + 1, c) : A, v1);
+      }
+    }
+  };
+  stage(0);
+  double nb0 = (rok && 2 * t < n) ? B[rlt_off<PM>(ldb, r, 2 * t)] : 0.0;
+  double nb1 = (rok && 2 * t + 1 < n) ? B[rlt_off<PM>(ldb, r, 2 * t + 1)] : 0.0;
+  for (int J = 0; J < nt; ++J) {
+    cp_async_wait_all();
+    __syncthreads();  // rows of tile J staged; every warp is done with tile J-1's buffer
+    if (J + 1 < nt) stage(J + 1);
+    const double* ab = ab_base + (J & 1) * abs;
+    const uint32_t abu = smem_u32(ab);
+    const int ca = 8 * J + 2 * t, cb = ca + 1;
+    double acc0 = alpha * nb0, acc1 = alpha * nb1;
+    if (J + 1 < nt) {  // next tile's right-hand side, loaded under this tile's work
+      nb0 = (rok && ca + 8 < n) ? B[rlt_off<PM>(ldb, r, ca + 8)] : 0.0;
+      nb1 = (rok && cb + 8 < n) ? B[rlt_off<PM>(ldb, r, cb + 8)] : 0.0;
+    }
+    // ---- C -= X(:, 0:8J) A(J, 0:8J)^T ----
+    double e0 = 0.0, e1 = 0.0;  // second accumulator pair: two independent DMMA chains
+    int T2 = 0;
+    for (; T2 + 2 <= J; T2 += 2) {
+      double xa[4], bf[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xa[u] = lds64(xs + 8u * ((2 * T2 + u) * 32 + lane));
+        bf[u] = -lds64(abu + 8u * ab_idx(8 * T2 + 4 * u + t, g));
+      }
+      dmma(acc0, acc1, xa[0], bf[0]);
+      dmma(e0, e1, xa[2], bf[2]);
+      dmma(acc0, acc1, xa[1], bf[1]);
+      dmma(e0, e1, xa[3], bf[3]);
+    }
+    if (T2 < J) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double xa = lds64(xs + 8u * ((2 * T2 + u) * 32 + lane));
+        const double bf = -lds64(abu + 8u * ab_idx(8 * T2 + 4 * u + t, g));
+        dmma(acc0, acc1, xa, bf);
+      }
+    }
+    acc0 += e0;
+    acc1 += e1;
+    // ---- 8x8 diagonal block: lane (g, t) owns columns 2t, 2t+1 of row r ----
+    // la[l] = A(8J+2t, 8J+l), lb[l] = A(8J+2t+1, 8J+l); identity past n
+    double la[8], lb[8];
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      la[l] = (l <= 2 * t && ca < n) ? ab[ab_idx(8 * J + l, 2 * t)] : (l == 2 * t ? 1.0 : 0.0);
+      lb[l] = (l <= 2 * t + 1 && cb < n) ? ab[ab_idx(8 * J + l, 2 * t + 1)] : (l == 2 * t + 1 ? 1.0 : 0.0);
+    }
+    const double da = ca < n ? ab[ab_idx(ca, 2 * t)] : 1.0;  // diagonal (nonzero: checked above)
+    const double db = cb < n ? ab[ab_idx(cb, 2 * t + 1)] : 1.0;
+    const double ra = L.unit ? 1.0 : __drcp_rn(da);
+    const double rbv = L.unit ? 1.0 : __drcp_rn(db);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int owner = c >> 1;
+      double xc;
+      if (c & 1) {
+        if (t == owner) acc1 *= rbv;
+        xc = __shfl_sync(0xffffffffu, acc1, (lane & ~3) | owner);
+      } else {
+        if (t == owner) acc0 *= ra;
+        xc = __shfl_sync(0xffffffffu, acc0, (lane & ~3) | owner);
+      }
+      // columns right of c: acc -= x(r, c) * A(col, c)
+      if (2 * t > c) acc0 = fma(-xc, la[c], acc0);
+      if (2 * t + 1 > c) acc1 = fma(-xc, lb[c], acc1);
+    }
+    if (rok && ca < n) D[rlt_off<PM>(ldd, r, ca)] = acc0;
+    if (rok && cb < n) D[rlt_off<PM>(ldd, r, cb)] = acc1;
+    // ---- re-lay as A fragments: kk = 0 needs column t, kk = 1 column 4 + t ----
+    const int src0 = (lane & ~3) | (t >> 1), src1 = (lane & ~3) | (2 + (t >> 1));
+    const double v00 = __shfl_sync(0xffffffffu, acc0, src0), v01 = __shfl_sync(0xffffffffu, acc1, src0);
+    const double v10 = __shfl_sync(0xffffffffu, acc0, src1), v11 = __shfl_sync(0xffffffffu, acc1, src1);
+    sts64(xs + 8u * ((2 * J) * 32 + lane), (t & 1) ? v01 : v00);
+    sts64(xs + 8u * ((2 * J + 1) * 32 + lane), (t & 1) ? v11 : v10);
+    __syncwarp();
+  }
+  cp_async_wait_all();
+  if (rb == 0 && lane == 0 && L.info && !L.skip_nonzero) L.info[p] = 0;
+}
+
+bool trsm_rlt_ok(const TrsmLaunch& L) { return !L.twin && L.lower && L.trans && L.nn <= 512; }
+
+cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
+  if (L.batch <= 0 || L.mm <= 0 || L.nn <= 0) return cudaSuccess;
+  RltArgs R;
+  R.L = L;
+  R.ntmax = (L.nn + 7) / 8;
+  R.rbmax = L.nvec ? R.ntmax : (L.mm + 7) / 8;
+  const size_t smem = (size_t)(kRltWarps + 2) * R.ntmax * 64 * sizeof(double);  // X slices + 2 staged A rows
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(trsm_rlt_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(trsm_rlt_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const unsigned grid = (unsigned)((long long)L.batch * ((R.rbmax + kRltWarps - 1) / kRltWarps));
+  if (L.pm)
+    trsm_rlt_kernel<1><<<grid, 32 * kRltWarps, smem, s>>>(R);
+  else
+    trsm_rlt_kernel<0><<<grid, 32 * kRltWarps, smem, s>>>(R);
+  return cudaGetLastError();
+}
+
+}  // namespace pbg

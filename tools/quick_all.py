@@ -66,3 +66,17 @@ if 'chain' in what:
         ms = timeit(f, 2)
         fl = float(sum(2 * int(n)**3 + int(n)**3 // 3 for n in ns))
         print(f"chain {layout}: {ms:.3f} ms (incl. C reset copy) {fl/ms/1e9:.2f} TF  info0={int(info.abs().sum())==0}")
+if 'trsm' in what:
+    for n in (32, 64, 128, 256):
+        batch = max(256, (2**30) // (16 * n * n))
+        Lm = torch.tril(torch.rand((batch, n, n), device=dev, dtype=torch.float64)) + n * torch.eye(n, device=dev, dtype=torch.float64)
+        Lc = Lm.transpose(1, 2).contiguous()  # column-major storage of L
+        B0 = torch.rand((batch, n, n), device=dev, dtype=torch.float64)
+        Bs = [B0.clone() for _ in range(3)]
+        it = iter(range(100))
+        tinfo = torch.empty(batch, dtype=torch.int32, device=dev)
+        f = lambda: pb.dtrsm_batched('r', 'l', 't', 'n', n, n, 1.0, Lc, n, n * n, Bs[next(it) % 3], n, n * n, tinfo, batch, stream=s)
+        ms = timeit(f)
+        fl = n ** 3 * batch; by = (8 * n * (n + 1) / 2 + 16 * n * n) * batch
+        roof = min(P, BW * fl / by)
+        print(f"trsm rltn n={n} batch={batch}: {ms:.4f} ms {fl/ms/1e9:.2f} TF roofline-frac {fl/(ms*1e-3)/roof:.3f}")
