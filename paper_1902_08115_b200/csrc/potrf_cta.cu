@@ -180,6 +180,48 @@ __device__ __forceinline__ int cta_factor_panel(uint32_t pan, int RS, int rows, 
   return 0;
 }
 
+// Broadcast variant: the diagonal block's rows are lanes 0..7 (slot 0); per
+// column they publish their entry of column c to a shared double buffer and
+// every lane reads the pivot and the multipliers back as broadcast loads, so
+// the 8x8 block is factored once instead of redundantly in every lane.
+template <int R>
+__device__ __forceinline__ int cta_factor_panel_bc(uint32_t pan, int RS, int rows, int lane, int gcol0, int n,
+                                                   uint32_t colbuf) {
+  double x[R][8];
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[q][c] = lds64(pan + 8u * (c * RS + lane + 32 * q));
+  double dsum = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint32_t cb = colbuf + (c & 1) * 64;
+    if (lane >= c && lane < 8) sts64(cb + 8u * lane, x[0][c]);
+    __syncwarp();
+    double col[8];
+#pragma unroll
+    for (int c2 = c & ~1; c2 < 8; c2 += 2) lds128(cb + 8u * c2, col[c2], col[c2 + 1]);
+    const double piv = col[c];
+    const double inv = rsqrt_nb(piv);
+    dsum += piv * inv;  // non-finite for a failed, denormal, +inf or NaN pivot
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      x[q][c] *= inv;
+      const double tq = x[q][c] * inv;
+#pragma unroll
+      for (int c2 = c + 1; c2 < 8; ++c2) x[q][c2] = fma(-tq, col[c2], x[q][c2]);
+    }
+  }
+  if (!(dsum <= 1.7976931348623157e308))  // warp-uniform
+    return cta_factor_panel_exact(pan, RS, rows, lane, gcol0, n);
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      sts64_if(pan + 8u * (c * RS + lane + 32 * q), x[q][c], lane + 32 * q < rows && (q > 0 || lane >= c));
+  return 0;
+}
+
 // Update warp: column block k1's tiles I = uw + NU*s (s < NS) accumulate
 // -sum_l L(I, l) L(k1, l)^T over l < k1 (panel k1-1 after its publication),
 // then go back to shared memory.  Returns true when the panel warp reported
@@ -281,6 +323,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   static_assert(SLOTS <= 11, "cta_update_block dispatch covers at most 11 tiles");
   extern __shared__ __align__(1024) double sm[];
   __shared__ int sh_fail, sh_rot;
+  __shared__ __align__(16) double sh_col[2][8];  // panel warp's column broadcast
   __shared__ __align__(8) uint64_t sh_bar[T];  // one per column panel (streamed staging)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const long long p = blockIdx.x;
@@ -441,7 +484,11 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       if (lane == 0) { PB_STAMP(4 + 2 * k) }
       const int RS = cta_pstride(T, k), rows = 8 * (TT - k);
       if (streamed || P.tma) mbar_wait(&sh_bar[k], 0);
+#ifdef PB_PANEL_REDUNDANT
       const int f = cta_factor_panel<R>(sbase + 8u * cta_pbase(T, k), RS, rows, lane, 8 * k, n);
+#else
+      const int f = cta_factor_panel_bc<R>(sbase + 8u * cta_pbase(T, k), RS, rows, lane, 8 * k, n, smem_u32(&sh_col[0][0]));
+#endif
       if (f && lane == 0) sh_fail = 8 * k + f;
       if (lane == 0) { PB_STAMP(5 + 2 * k) }
       named_sync(1, NTH);  // panel k published (or the failure flag)
