@@ -222,7 +222,7 @@ def time_device(fn, steps, warmup, stream, ws):
     return e0.elapsed_time(e1)
 
 
-def series_dpotrf(pb, dev, stream):
+def series_dpotrf(pb, dev, stream, peak_tf, bw):
     """dpotrf_l (config 3) GFLOP/s at each n: inputs SPD = B B^T + n I, B ~ N(0,1)."""
     import torch
     out = {}
@@ -251,8 +251,115 @@ def series_dpotrf(pb, dev, stream):
         flops = (n * n * n // 3) * batch
         gf = flops / ms / 1e6
         by = 8 * n * (n + 1) * batch
-        out[str(n)] = {"gflops": round(gf, 1), "ms": round(ms, 4), "hbm_gbs": round(by / ms / 1e6, 1)}
+        roof = batch * _roof(n * n * n // 3, 8 * n * (n + 1), peak_tf, bw)
+        out[str(n)] = {"gflops": round(gf, 1), "ms": round(ms, 4), "hbm_gbs": round(by / ms / 1e6, 1),
+                       "roofline_frac": round(roof * 1e3 / ms, 3)}
         del A, A0
+    return out
+
+
+def _roof(flops, bytes_, peak_tf, bw):
+    """FP64 roofline time (s) of one problem: max(flops / P, bytes / BW)."""
+    return max(flops / (peak_tf * 1e12), bytes_ / (bw * 1e9))
+
+
+def _median_ms(fn, stream, reps=3, setup=None):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    laps = []
+    for r in range(reps + 1):
+        if setup:
+            setup()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if r:
+            laps.append(e0.elapsed_time(e1))
+    return statistics.median(laps)
+
+
+def series_gemm_nd(pb, dev, stream, peak_tf, bw):
+    """Config 2: gemm_nd NT on panel-major (ps = 4) operands, batch(s) = 2^31 / (32 s^2)."""
+    import torch
+    out = {}
+    for s_ in (4, 8, 16, 24, 32, 48, 64, 96, 128, 192, 256, 320):
+        batch = (2 ** 31) // (32 * s_ * s_)
+        L = s_ * s_
+        A = torch.rand((batch, L), device=dev, dtype=torch.float64)
+        B = torch.rand_like(A); C = torch.rand_like(A); D = torch.empty_like(A)
+        R = pb.PanelRef
+        fn = lambda: pb.gemm_nd_batched("n", "t", s_, s_, s_, 1.0, R(A, s_, s_), L, R(B, s_, s_), L, 1.0,
+                                        R(C, s_, s_), L, R(D, s_, s_), L, batch, stream=stream)
+        ms = _median_ms(fn, stream)
+        fl = 2 * s_ ** 3 * batch
+        roof = batch * _roof(2 * s_ ** 3, 32 * s_ * s_, peak_tf, bw)
+        out[str(s_)] = {"gflops": round(fl / ms / 1e6, 1), "ms": round(ms, 4), "batch": batch,
+                        "roofline_frac": round(roof * 1e3 / ms, 3)}
+        del A, B, C, D
+    return out
+
+
+def series_dgetrf(pb, dev, stream, peak_tf, bw):
+    """Config 4: dgetrf with partial pivoting, uniform[-1,1], batch 8192."""
+    import torch
+    out = {}
+    g = torch.Generator(device=dev).manual_seed(4)
+    for n in (24, 48, 96, 192):
+        batch = 8192
+        A0 = torch.rand((batch, n, n), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+        A = A0.clone()
+        ip = torch.empty((batch, n), dtype=torch.int32, device=dev)
+        info = torch.empty(batch, dtype=torch.int32, device=dev)
+        ms = _median_ms(lambda: pb.dgetrf_batched(n, n, A, n, n * n, ip, n, info, batch, stream=stream), stream,
+                        setup=lambda: A.copy_(A0))
+        fpp = n ** 3 - n ** 3 // 3
+        roof = batch * _roof(fpp, 16 * n * n + 4 * n, peak_tf, bw)
+        out[str(n)] = {"gflops": round(fpp * batch / ms / 1e6, 1), "ms": round(ms, 4),
+                       "roofline_frac": round(roof * 1e3 / ms, 3)}
+        del A, A0
+    return out
+
+
+def series_chain(pb, dev, stream, peak_tf, bw):
+    """Config 5: 32768 problems, n = 4 U{1..64}: dsyrk_ln -> dpotrf_l -> dtrsm_rltn, cm and pm."""
+    import numpy as np
+    import torch
+    rng = np.random.default_rng(5)
+    batch = 32768
+    ns = rng.integers(1, 65, batch) * 4
+    offs = np.concatenate([[0], np.cumsum(ns.astype(np.int64) ** 2)[:-1]])
+    total = int((ns.astype(np.int64) ** 2).sum())
+    fl = float(sum(2 * int(n) ** 3 + int(n) ** 3 // 3 for n in ns))
+    roof = float(sum(_roof(2 * int(n) ** 3 + int(n) ** 3 // 3, 8 * (3 * int(n) ** 2 + int(n) * (int(n) + 1)),
+                           peak_tf, bw) for n in ns))
+    out = {}
+    dn = torch.from_numpy(ns.astype(np.int32)).to(dev)
+    doff = torch.from_numpy(offs).to(dev)
+    info = torch.empty(batch, dtype=torch.int32, device=dev)
+    for layout in "CP":
+        A = torch.rand(total, device=dev, dtype=torch.float64) * 2 - 1
+        B0 = torch.rand(total, device=dev, dtype=torch.float64) * 2 - 1
+        C0 = torch.zeros(total, device=dev, dtype=torch.float64)
+        for n in np.unique(ns):  # C0 = n I
+            idx = np.nonzero(ns == n)[0]
+            base = torch.from_numpy(offs[idx]).to(dev)
+            ar = torch.arange(int(n), device=dev)
+            diag = ar * (int(n) + 1) if layout == "C" else (ar // 4) * 4 * int(n) + ar * 4 + ar % 4
+            C0[(base[:, None] + diag[None, :]).reshape(-1)] = float(n)
+        C = C0.clone(); B = B0.clone()
+
+        def setup():
+            C.copy_(C0); B.copy_(B0)
+
+        ms = _median_ms(lambda: pb.chain_vbatched(layout, dn, doff, A, C, B, info, batch, 256, stream=stream),
+                        stream, reps=2, setup=setup)
+        assert int(info.abs().sum()) == 0
+        out["cm" if layout == "C" else "pm"] = {"gflops": round(fl / ms / 1e6, 1), "ms": round(ms, 3),
+                                                "roofline_frac": round(roof * 1e3 / ms, 3)}
+        del A, B0, C0, C, B
     return out
 
 
@@ -362,8 +469,17 @@ def run_gpu_arm(args, ws, rank, local):
                                 "sample": f"{sample} of the cfg1 problems, median of 3 passes "
                                           f"({sec:.2f} s each), {threads} threads contiguous split"}
     if rank == 0 and ws == 1 and not args.no_series:
-        line["series"] = {"dgemm_nn_cm": series_dgemm(pb, dev, stream),
-                          "dpotrf_l": series_dpotrf(pb, dev, stream)}
+        del A, B, C
+        torch.cuda.empty_cache()
+        bw, _ = measured_peaks()
+        peak = pb.lib().pb_probe_dmma_tflops()
+        line["series"] = {"roofline": f"per problem max(flops / {peak:.2f} TFLOP/s measured DMMA, "
+                                      f"algorithmic bytes / {bw} GB/s), summed over the batch",
+                          "cfg1_dgemm_nn_cm": series_dgemm(pb, dev, stream),
+                          "cfg2_gemm_nd_nt_pm": series_gemm_nd(pb, dev, stream, peak, bw),
+                          "cfg3_dpotrf_l": series_dpotrf(pb, dev, stream, peak, bw),
+                          "cfg4_dgetrf": series_dgetrf(pb, dev, stream, peak, bw),
+                          "cfg5_chain": series_chain(pb, dev, stream, peak, bw)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
