@@ -219,9 +219,13 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
   }();
   if (!legacy && getrf_reg_ok(L.m, L.n))
     return getrf_reg_launch(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, L.batch, s);
-  if (fits_smem(L.m, L.n) && !legacy && L.m <= 224)
+  static const int blocked_from = [] {  // PBGPU_GETRF_BLOCKED_FROM=n: blocked path from this order on (tuning)
+    const char* e = getenv("PBGPU_GETRF_BLOCKED_FROM");
+    return e ? atoi(e) : 80;
+  }();
+  if (fits_smem(L.m, L.n) && !legacy && L.m <= 224 && std::min(L.m, L.n) < blocked_from)
     return getrf_cta_launch(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, 0, 0, L.batch, s);
-  if (fits_smem(L.m, L.n))
+  if (fits_smem(L.m, L.n) && std::min(L.m, L.n) < blocked_from)
     return getrf_smem(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, 0, 0, L.batch, s);
   // Blocked right-looking LU over tall panels of nb columns.
   const int minmn = std::min(L.m, L.n);
@@ -229,15 +233,20 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
   while (nb > 8 && !fits_smem(L.m, nb)) nb /= 2;
   if (!fits_smem(L.m, nb)) return cudaErrorInvalidValue;
   if (fits_smem(L.m, 96) && L.n <= 192) nb = 96;
-  const bool rows = !legacy && getrf_rows_ok(L.m, 64);
-  if (rows) nb = 64;  // tall panels on the row-resident kernel
+  static const int nb_env = [] {  // PBGPU_GETRF_NB: tall-panel width of the row-resident path (tuning)
+    const char* e = getenv("PBGPU_GETRF_NB");
+    return e ? atoi(e) : 0;
+  }();
+  const int nbr = nb_env == 16 || nb_env == 48 || nb_env == 64 ? nb_env : 32;  // 32 measured best (n = 96, 192)
+  const bool rows = !legacy && getrf_rows_ok(L.m, nbr);
+  if (rows) nb = nbr;  // tall panels on the row-resident kernel
   for (int j0 = 0; j0 < minmn; j0 += nb) {
     const int jb = std::min(nb, minmn - j0);
     const int mm = L.m - j0;
     double* panel = L.a + (long long)j0 + (long long)j0 * L.lda;
     // 1. factor the tall panel rows j0.., cols j0..j0+jb (pivots offset by j0)
     cudaError_t e = rows ? getrf_rows_launch(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info, j0,
-                                             j0 > 0, L.batch, s)
+                                             j0 > 0, L.batch, j0, L.n, s)
                     : (!legacy && mm <= 224)
                         ? getrf_cta_launch(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info, j0,
                                            j0 > 0, L.batch, s)
@@ -245,16 +254,19 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
                                      j0 > 0, L.batch, s);
     if (e != cudaSuccess) return e;
     // 2. apply the panel's interchanges to the columns left and right of it
+    //    (the row-resident panel kernel already moved whole rows)
     dim3 grid(std::max(1, (std::max(j0, L.n - j0 - jb) + 127) / 128), L.batch);
-    if (j0 > 0) {
+    if (j0 > 0 && !rows) {
       laswp_kernel<<<grid, 128, 0, s>>>(L.a, L.stride, L.lda, L.ipiv, L.stride_ipiv, j0, j0 + jb, 0, j0);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     const int nw = L.n - j0 - jb;
     if (nw <= 0) continue;
-    laswp_kernel<<<grid, 128, 0, s>>>(L.a, L.stride, L.lda, L.ipiv, L.stride_ipiv, j0, j0 + jb,
-                                      j0 + jb, L.n);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (!rows) {
+      laswp_kernel<<<grid, 128, 0, s>>>(L.a, L.stride, L.lda, L.ipiv, L.stride_ipiv, j0, j0 + jb,
+                                        j0 + jb, L.n);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     // 3. U12 = L11^{-1} A12 (left, lower, no-trans, unit) = transposed right-side problem
     double* a12 = L.a + (long long)j0 + (long long)(j0 + jb) * L.lda;
     TrsmLaunch T;

@@ -39,6 +39,9 @@ struct GetrfRowsArgs {
   int piv_offset;
   int keep_info;  // keep an info already set by an earlier panel
   int batch;
+  // tall panels of the blocked path: the panel is columns [col0, col0 + n) of a
+  // matrix with ncols columns; its interchanges are applied to all the others
+  int col0, ncols;
 };
 
 template <int N, int NW>
@@ -122,6 +125,30 @@ __global__ void __launch_bounds__(32 * NW) getrf_rows_kernel(const __grid_consta
   }
 #pragma unroll
   for (int j = 0; j < N; ++j) stg_if(a + pos + j * lda, x[j], r < m && j < n);
+  // the panel's interchanges on the other columns of the rows (LAPACK applies
+  // them to the whole row; the reference, factor.hpp:175-183): every row moves
+  // from its original position to its final one, 16 columns per round, reads
+  // and writes separated by barriers (the moves form a permutation)
+  if (P.ncols > n) {
+    const bool mv = r < m && pos != r;
+    const int lo = -P.col0, hi = P.ncols - P.col0;  // column range relative to the panel
+    for (int q0 = lo; q0 < hi; q0 += 16) {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int q = q0 + u;
+        const bool ok = mv && q < hi && (q < 0 || q >= n);
+        v[u] = ldg_if(a + r + (long long)q * lda, ok, 0.0);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int q = q0 + u;
+        stg_if(a + pos + (long long)q * lda, v[u], mv && q < hi && (q < 0 || q >= n));
+      }
+      __syncthreads();
+    }
+  }
   if (tid < minmn) P.ipiv[p * P.sp + tid] = my_ipiv;
   if (tid == 0) {
     const int fz = first_zero ? first_zero + P.piv_offset : 0;
@@ -138,11 +165,31 @@ static cudaError_t rows_t(const GetrfRowsArgs& P, cudaStream_t s) {
 bool getrf_rows_ok(int m, int n) { return m >= 1 && n >= 1 && m <= 224 && n <= 96 && !(n > 64 && m > 96); }
 
 cudaError_t getrf_rows_launch(double* a, long long stride, int lda, int m, int n, int* ipiv, long long sp, int* info,
-                              int piv_offset, int keep_info, int batch, cudaStream_t s) {
+                              int piv_offset, int keep_info, int batch, int col0, int ncols, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
-  GetrfRowsArgs P{a, stride, lda, m, n, ipiv, sp, info, piv_offset, keep_info, batch};
+  GetrfRowsArgs P{a, stride, lda, m, n, ipiv, sp, info, piv_offset, keep_info, batch, col0, ncols};
   const int nw = (m + 31) / 32;
-  if (n <= 48) {
+  if (n <= 16) {
+    switch (nw) {
+      case 1: return rows_t<16, 1>(P, s);
+      case 2: return rows_t<16, 2>(P, s);
+      case 3: return rows_t<16, 3>(P, s);
+      case 4: return rows_t<16, 4>(P, s);
+      case 5: return rows_t<16, 5>(P, s);
+      case 6: return rows_t<16, 6>(P, s);
+      case 7: return rows_t<16, 7>(P, s);
+    }
+  } else if (n <= 32) {
+    switch (nw) {
+      case 1: return rows_t<32, 1>(P, s);
+      case 2: return rows_t<32, 2>(P, s);
+      case 3: return rows_t<32, 3>(P, s);
+      case 4: return rows_t<32, 4>(P, s);
+      case 5: return rows_t<32, 5>(P, s);
+      case 6: return rows_t<32, 6>(P, s);
+      case 7: return rows_t<32, 7>(P, s);
+    }
+  } else if (n <= 48) {
     switch (nw) {
       case 1: return rows_t<48, 1>(P, s);
       case 2: return rows_t<48, 2>(P, s);

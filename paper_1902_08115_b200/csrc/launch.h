@@ -122,8 +122,10 @@ cudaError_t getrf_reg_launch(double* a, long long stride, int lda, int m, int n,
 // row-resident CTA-per-problem LU, m <= 224 and n <= 64 (n <= 96 for m <= 96)
 // (getrf_rows.cu); piv_offset / keep_info serve the tall panels of the blocked path
 bool getrf_rows_ok(int m, int n);
+// col0/ncols: the panel is columns [col0, col0 + n) of an ncols-column matrix and its
+// interchanges are applied to every other column (ncols <= n: panel only)
 cudaError_t getrf_rows_launch(double* a, long long stride, int lda, int m, int n, int* ipiv, long long sp, int* info,
-                              int piv_offset, int keep_info, int batch, cudaStream_t s);
+                              int piv_offset, int keep_info, int batch, int col0, int ncols, cudaStream_t s);
 
 // Triangular solve.  Column-major dtrsm (in place on b) or the panel-major
 // trsm_rltn_nd (b -> d, d may alias b).  The effective problem is always a
