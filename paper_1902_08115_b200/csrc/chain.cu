@@ -122,6 +122,7 @@ cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
 // ------------------------------------------------------------------ chain (cfg 5)
 cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
   if (L.batch <= 0) return cudaSuccess;
+  mempool_keep();
   cudaError_t e;
   // The split by order is planned on the host.
   std::vector<int> nv(L.batch);

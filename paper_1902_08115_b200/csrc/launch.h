@@ -159,6 +159,8 @@ cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s);
 // warp-per-8-rows left-looking DMMA solve for X * A^T = alpha B, A lower (trsm_rlt.cu);
 // trsm_launch forwards these flag sets
 bool trsm_rlt_ok(const TrsmLaunch& L);
+// keep the default stream-ordered memory pool's memory between calls (scratch reuse)
+void mempool_keep();
 cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s);
 
 // Fused panel-major lower chol(C + A B^T) (syrk_potrf_nd).

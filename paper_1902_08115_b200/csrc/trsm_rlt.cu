@@ -32,12 +32,59 @@ struct RltArgs {
   TrsmLaunch L;
   int rbmax;  // row blocks (8 rows) per problem slot in the grid
   int ntmax;  // column tiles of the largest problem (shared-memory slice)
+  double* W;  // inverses of the 8x8 diagonal blocks, [problem][tile][kk][lane] (B-fragment order)
 };
 
 template <int PM>
 __device__ __forceinline__ long long rlt_off(long long ld, int r, int c) {
   if (PM) return (long long)(r >> 2) * 4 * ld + (long long)c * 4 + (r & 3);
   return (long long)r + (long long)c * ld;
+}
+
+// Inverses of the 8x8 diagonal blocks of A, one thread per (problem, tile,
+// column j): forward substitution L y = e_j with reciprocal multiplies
+// (identity past n; a unit diagonal is taken as 1).  Stored where lane
+// (g, t) of the solve reads its B fragment inv(L)[g][4 kk + t].
+template <int PM>
+__global__ void __launch_bounds__(256) diag_inv8_kernel(const __grid_constant__ RltArgs R) {
+  const TrsmLaunch& L = R.L;
+  const long long e = (long long)blockIdx.x * 256 + threadIdx.x;
+  const long long p = e / (R.ntmax * 8);
+  if (p >= L.batch) return;
+  const int rem = (int)(e - p * R.ntmax * 8), J = rem >> 3, j = rem & 7;
+  int n = L.nn;
+  long long lda = L.lda;
+  const double* A;
+  if (L.nvec) {
+    n = L.nvec[p];
+    lda = PM ? ((n + 3) & ~3) : n;
+    A = L.a + L.offs[p];
+  } else {
+    A = L.a + p * L.sa;
+  }
+  if (8 * J >= n) return;
+  auto el = [&](int i, int l) -> double {  // L_JJ(i, l), l <= i
+    const int r = 8 * J + i, c = 8 * J + l;
+    if (r >= n || c >= n) return i == l ? 1.0 : 0.0;
+    if (i == l && L.unit) return 1.0;
+    return A[rlt_off<PM>(lda, r, c)];
+  };
+  double y[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i < j) {
+      y[i] = 0.0;
+    } else {
+      double acc = i == j ? 1.0 : 0.0;
+#pragma unroll
+      for (int l = 0; l < i; ++l)
+        if (l >= j) acc = fma(-el(i, l), y[l], acc);
+      y[i] = acc * __drcp_rn(el(i, i));
+    }
+  }
+  double* w = R.W + (p * R.ntmax + J) * 64 + (j >> 2) * 32 + (j & 3);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) w[4 * i] = y[i];
 }
 
 // Staged rows of A: column c of the 8-row block at c*8, rows XOR-swizzled so
@@ -146,32 +193,16 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     }
     acc0 += e0;
     acc1 += e1;
-    // ---- 8x8 diagonal block: lane (g, t) owns columns 2t, 2t+1 of row r ----
-    // la[l] = A(8J+2t, 8J+l), lb[l] = A(8J+2t+1, 8J+l); identity past n
-    double la[8], lb[8];
-#pragma unroll
-    for (int l = 0; l < 8; ++l) {
-      la[l] = (l <= 2 * t && ca < n) ? ab[ab_idx(8 * J + l, 2 * t)] : (l == 2 * t ? 1.0 : 0.0);
-      lb[l] = (l <= 2 * t + 1 && cb < n) ? ab[ab_idx(8 * J + l, 2 * t + 1)] : (l == 2 * t + 1 ? 1.0 : 0.0);
-    }
-    const double da = ca < n ? ab[ab_idx(ca, 2 * t)] : 1.0;  // diagonal (nonzero: checked above)
-    const double db = cb < n ? ab[ab_idx(cb, 2 * t + 1)] : 1.0;
-    const double ra = L.unit ? 1.0 : __drcp_rn(da);
-    const double rbv = L.unit ? 1.0 : __drcp_rn(db);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int owner = c >> 1;
-      double xc;
-      if (c & 1) {
-        if (t == owner) acc1 *= rbv;
-        xc = __shfl_sync(0xffffffffu, acc1, (lane & ~3) | owner);
-      } else {
-        if (t == owner) acc0 *= ra;
-        xc = __shfl_sync(0xffffffffu, acc0, (lane & ~3) | owner);
-      }
-      // columns right of c: acc -= x(r, c) * A(col, c)
-      if (2 * t > c) acc0 = fma(-xc, la[c], acc0);
-      if (2 * t + 1 > c) acc1 = fma(-xc, lb[c], acc1);
+    // ---- 8x8 diagonal block: X = C inv(L_JJ)^T on the tensor cores (C re-laid as A fragments) ----
+    {
+      const int s0 = (lane & ~3) | (t >> 1), s1 = (lane & ~3) | (2 + (t >> 1));
+      const double u00 = __shfl_sync(0xffffffffu, acc0, s0), u01 = __shfl_sync(0xffffffffu, acc1, s0);
+      const double u10 = __shfl_sync(0xffffffffu, acc0, s1), u11 = __shfl_sync(0xffffffffu, acc1, s1);
+      const double* w = R.W + (p * R.ntmax + J) * 64 + lane;
+      const double w0 = w[0], w1 = w[32];
+      acc0 = acc1 = 0.0;
+      dmma(acc0, acc1, (t & 1) ? u01 : u00, w0);
+      dmma(acc0, acc1, (t & 1) ? u11 : u10, w1);
     }
     if (rok && ca < n) D[rlt_off<PM>(ldd, r, ca)] = acc0;
     if (rok && cb < n) D[rlt_off<PM>(ldd, r, cb)] = acc1;
@@ -185,6 +216,22 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
   }
   cp_async_wait_all();
   if (rb == 0 && lane == 0 && L.info && !L.skip_nonzero) L.info[p] = 0;
+}
+
+// Stream-ordered scratch (cudaMallocAsync) stays cheap only if the default
+// pool keeps its memory between calls instead of releasing it at every
+// synchronization: raise the release threshold once per device.
+void mempool_keep() {
+  static int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done_dev = dev;
 }
 
 bool trsm_rlt_ok(const TrsmLaunch& L) { return !L.twin && L.lower && L.trans && L.nn <= 512; }
@@ -205,11 +252,20 @@ cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
     attr = true;
   }
   const unsigned grid = (unsigned)((long long)L.batch * ((R.rbmax + kRltWarps - 1) / kRltWarps));
-  if (L.pm)
+  mempool_keep();
+  cudaError_t e = cudaMallocAsync(&R.W, sizeof(double) * 64 * R.ntmax * (size_t)L.batch, s);
+  if (e != cudaSuccess) return e;
+  const unsigned igrid = (unsigned)(((long long)L.batch * R.ntmax * 8 + 255) / 256);
+  if (L.pm) {
+    diag_inv8_kernel<1><<<igrid, 256, 0, s>>>(R);
     trsm_rlt_kernel<1><<<grid, 32 * kRltWarps, smem, s>>>(R);
-  else
+  } else {
+    diag_inv8_kernel<0><<<igrid, 256, 0, s>>>(R);
     trsm_rlt_kernel<0><<<grid, 32 * kRltWarps, smem, s>>>(R);
-  return cudaGetLastError();
+  }
+  e = cudaGetLastError();
+  cudaFreeAsync(R.W, s);
+  return e;
 }
 
 }  // namespace pbg

@@ -34,6 +34,16 @@ elif what == "getrf":
         pb.dgetrf_batched(n, n, A, n, n * n, ipiv, n, info, batch)
 torch.cuda.synchronize()
 print("done", what, n)
+if what == "gemm_nd":
+    batch = (2 ** 31) // (32 * n * n)
+    L = n * n
+    A = torch.rand((batch, L), device=dev, dtype=torch.float64)
+    B = torch.rand_like(A); C = torch.rand_like(A); D = torch.empty_like(A)
+    R = pb.PanelRef
+    for _ in range(reps):
+        pb.gemm_nd_batched("n", "t", n, n, n, 1.0, R(A, n, n), L, R(B, n, n), L, 1.0, R(C, n, n), L, R(D, n, n), L, batch)
+    torch.cuda.synchronize()
+    print("done gemm_nd", n)
 if what == "trsm":
     batch = max(256, (2**30) // (16 * n * n))
     Lm = torch.tril(torch.rand((batch, n, n), device=dev, dtype=torch.float64)) + n * torch.eye(n, device=dev, dtype=torch.float64)
