@@ -119,6 +119,48 @@ __global__ void __launch_bounds__(32 * SM_WARPS) gemm_small_kernel(const __grid_
   if (tid == 0) bulk_wait_read0();
 }
 
+// s = 4: a problem is one 4x4 panel (element (i, l) at l*4 + i), 128 bytes per
+// operand.  One thread owns one problem: 16-byte streaming loads of A, B (and
+// C), 64 FMAs in registers, 16-byte stores — the problem is pure HBM traffic
+// and needs no shared memory or tensor cores.
+__global__ void __launch_bounds__(256) gemm_tiny4_kernel(const __grid_constant__ SmallArgs P) {
+  const long long p = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (p >= P.batch) return;
+  const double2* A = reinterpret_cast<const double2*>(P.a + p * 16);
+  const double2* B = reinterpret_cast<const double2*>(P.b + p * 16);
+  double a[16], b[16];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const double2 va = __ldcs(A + u), vb = __ldcs(B + u);
+    a[2 * u] = va.x; a[2 * u + 1] = va.y;
+    b[2 * u] = vb.x; b[2 * u + 1] = vb.y;
+  }
+  double c[16];
+  const bool use_c = P.beta != 0.0;
+  if (use_c) {
+    const double2* C = reinterpret_cast<const double2*>(P.c + p * 16);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double2 v = __ldcs(C + u);
+      c[2 * u] = v.x; c[2 * u + 1] = v.y;
+    }
+  }
+  double2* D = reinterpret_cast<double2*>(P.d + p * 16);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {    // column j of D = row j of B
+    double out[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // D(i, j) = sum_l A(i, l) B(j, l)
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < 4; ++l) acc = fma(a[l * 4 + i], b[l * 4 + j], acc);
+      out[i] = use_c ? fma(P.alpha, acc, P.beta * c[j * 4 + i]) : P.alpha * acc;
+    }
+    __stcs(D + 2 * j, make_double2(out[0], out[1]));
+    __stcs(D + 2 * j + 1, make_double2(out[2], out[3]));
+  }
+}
+
 template <int T>
 static cudaError_t small_t(SmallArgs& P, cudaStream_t st) {
   const size_t smem = 2 * 3 * (size_t)P.G * P.s * P.s * sizeof(double);
@@ -152,6 +194,10 @@ cudaError_t gemm_small_launch(int s, double alpha, const double* a, const double
   // chunk: <= 16 KB per operand; two stages of A, B, C = 96 KB, two CTAs per SM
   P.G = std::max(1, 2048 / (s * s));
   P.nchunks = (int)((batch + P.G - 1) / P.G);
+  if (s == 4) {
+    gemm_tiny4_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(P);
+    return cudaGetLastError();
+  }
   switch ((s + 7) / 8) {
     case 1: return small_t<1>(P, st);
     case 2: return small_t<2>(P, st);

@@ -130,6 +130,37 @@ def test_gemm_nd_nt_batched(pb, orc, cuda, s):
         assert rel_frob(unpack(got[p], s, s), unpack(want, s, s)) <= tol(s)
 
 
+@pytest.mark.parametrize("s", [4, 8, 16, 32])
+def test_gemm_nd_small_alpha_beta_alias(pb, orc, cuda, s):
+    """Small-size branch: beta == 0 never reads C (NaN C), alpha scaling, D aliasing C."""
+    import torch
+    rng = np.random.default_rng(300 + s)
+    batch = 37
+    L = panel_len(s, s)
+    A = rng.uniform(-1, 1, (batch, L)); B = rng.uniform(-1, 1, (batch, L)); Cp = rng.uniform(-1, 1, (batch, L))
+    dA, dB = (torch.from_numpy(x.copy()).to(cuda) for x in (A, B))
+    dC = torch.full((batch, L), float("nan"), device=cuda, dtype=torch.float64)
+    dD = torch.empty((batch, L), device=cuda, dtype=torch.float64)
+    R = pb.PanelRef
+    assert pb.gemm_nd_batched("n", "t", s, s, s, -1.5, R(dA, s, s), L, R(dB, s, s), L, 0.0, R(dC, s, s), L,
+                              R(dD, s, s), L, batch).ok()
+    got = dD.cpu().numpy()
+    assert not np.isnan(got).any()
+    dIO = torch.from_numpy(Cp.copy()).to(cuda)  # in place: D aliases C, beta = 0.5
+    assert pb.gemm_nd_batched("n", "t", s, s, s, 1.0, R(dA, s, s), L, R(dB, s, s), L, 0.5, R(dIO, s, s), L,
+                              R(dIO, s, s), L, batch).ok()
+    io = dIO.cpu().numpy()
+    for p in range(0, batch, 6):
+        c_nan, want = np.full(L, np.nan), np.zeros(L)
+        orc.gemm_nd(b"n", b"t", s, s, s, -1.5, dmat(A[p], s, s), dmat(B[p], s, s), 0.0, dmat(c_nan, s, s),
+                    dmat(want, s, s))
+        assert rel_frob(unpack(got[p], s, s), unpack(want, s, s)) <= tol(s)
+        c_in, want2 = Cp[p].copy(), Cp[p].copy()
+        orc.gemm_nd(b"n", b"t", s, s, s, 1.0, dmat(A[p], s, s), dmat(B[p], s, s), 0.5, dmat(c_in, s, s),
+                    dmat(want2, s, s))
+        assert rel_frob(unpack(io[p], s, s), unpack(want2, s, s)) <= tol(s)
+
+
 def test_gemm_nd_odd_shapes_and_nn(pb, orc):
     rng = np.random.default_rng(21)
     for (m, n, k) in [(5, 7, 3), (9, 19, 13), (66, 70, 37)]:
