@@ -223,7 +223,7 @@ def time_device(fn, steps, warmup, stream, ws):
 
 
 def series_dpotrf(pb, dev, stream, peak_tf, bw):
-    """dpotrf_l (config 3) GFLOP/s at each n: inputs SPD = B B^T + n I, B ~ N(0,1)."""
+    """dpotrf_l (config 3) GFLOP/s at each n: inputs SPD = B B^T + n I, B ~ N(0,1); HBM-resident inputs."""
     import torch
     out = {}
     g = torch.Generator(device=dev).manual_seed(3)
@@ -232,29 +232,21 @@ def series_dpotrf(pb, dev, stream, peak_tf, bw):
         Bm = torch.randn((batch, n, n), generator=g, device=dev, dtype=torch.float64)
         A0 = Bm @ Bm.transpose(1, 2) + n * torch.eye(n, device=dev, dtype=torch.float64)
         del Bm
-        A = A0.clone()
         info = torch.empty(batch, dtype=torch.int32, device=dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        laps = []
-        for r in range(4):
-            A.copy_(A0)  # restore the pristine input outside the timed region
-            torch.cuda.synchronize()
-            e0.record(stream)
-            pb.dpotrf_batched("l", n, A, n, n * n, info, batch, stream=stream)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            if r:
-                laps.append(e0.elapsed_time(e1))
+
+        def make():
+            A = A0.clone()
+            return A, (lambda: A.copy_(A0))
+
+        ms, R = _time_copies(make, lambda A: pb.dpotrf_batched("l", n, A, n, n * n, info, batch, stream=stream),
+                             stream, A0.numel() * 8)
         assert int(info.abs().sum()) == 0
-        ms = statistics.median(laps)
         flops = (n * n * n // 3) * batch
-        gf = flops / ms / 1e6
         by = 8 * n * (n + 1) * batch
         roof = batch * _roof(n * n * n // 3, 8 * n * (n + 1), peak_tf, bw)
-        out[str(n)] = {"gflops": round(gf, 1), "ms": round(ms, 4), "hbm_gbs": round(by / ms / 1e6, 1),
-                       "roofline_frac": round(roof * 1e3 / ms, 3)}
-        del A, A0
+        out[str(n)] = {"gflops": round(flops / ms / 1e6, 1), "ms": round(ms, 4), "hbm_gbs": round(by / ms / 1e6, 1),
+                       "roofline_frac": round(roof * 1e3 / ms, 3), "launches_timed": R}
+        del A0
     return out
 
 
@@ -281,6 +273,33 @@ def _median_ms(fn, stream, reps=3, setup=None):
     return statistics.median(laps)
 
 
+def _time_copies(make_copy, launch, stream, footprint_bytes, l2_bytes=126 * 2 ** 20):
+    """Device time of one launch when inputs come from HBM: R back-to-back launches on R
+    distinct copies (R copies >= 2x L2), L2 flushed (a 512 MiB write) before the timed region;
+    returns ms per launch (median of 3)."""
+    import torch
+    R = max(4, min(64, int(2 * l2_bytes // max(1, footprint_bytes)) + 1))
+    copies = [make_copy() for _ in range(R)]
+    scratch = torch.empty(64 * 2 ** 20, dtype=torch.float64, device=copies[0][0].device)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    laps = []
+    for rep in range(4):
+        for c in copies:
+            c[1]()  # restore the pristine input
+        scratch.fill_(float(rep))  # L2 flush
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for c in copies:
+            launch(c[0])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if rep:
+            laps.append(e0.elapsed_time(e1) / R)
+    del copies, scratch
+    return statistics.median(laps), R
+
+
 def series_gemm_nd(pb, dev, stream, peak_tf, bw):
     """Config 2: gemm_nd NT on panel-major (ps = 4) operands, batch(s) = 2^31 / (32 s^2)."""
     import torch
@@ -303,23 +322,27 @@ def series_gemm_nd(pb, dev, stream, peak_tf, bw):
 
 
 def series_dgetrf(pb, dev, stream, peak_tf, bw):
-    """Config 4: dgetrf with partial pivoting, uniform[-1,1], batch 8192."""
+    """Config 4: dgetrf with partial pivoting, uniform[-1,1], batch 8192; HBM-resident inputs."""
     import torch
     out = {}
     g = torch.Generator(device=dev).manual_seed(4)
     for n in (24, 48, 96, 192):
         batch = 8192
         A0 = torch.rand((batch, n, n), generator=g, device=dev, dtype=torch.float64) * 2 - 1
-        A = A0.clone()
         ip = torch.empty((batch, n), dtype=torch.int32, device=dev)
         info = torch.empty(batch, dtype=torch.int32, device=dev)
-        ms = _median_ms(lambda: pb.dgetrf_batched(n, n, A, n, n * n, ip, n, info, batch, stream=stream), stream,
-                        setup=lambda: A.copy_(A0))
+
+        def make():
+            A = A0.clone()
+            return A, (lambda: A.copy_(A0))
+
+        ms, R = _time_copies(make, lambda A: pb.dgetrf_batched(n, n, A, n, n * n, ip, n, info, batch, stream=stream),
+                             stream, A0.numel() * 8)
         fpp = n ** 3 - n ** 3 // 3
         roof = batch * _roof(fpp, 16 * n * n + 4 * n, peak_tf, bw)
         out[str(n)] = {"gflops": round(fpp * batch / ms / 1e6, 1), "ms": round(ms, 4),
-                       "roofline_frac": round(roof * 1e3 / ms, 3)}
-        del A, A0
+                       "roofline_frac": round(roof * 1e3 / ms, 3), "launches_timed": R}
+        del A0
     return out
 
 
