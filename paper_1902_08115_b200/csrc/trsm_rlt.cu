@@ -20,6 +20,7 @@
 // (level3.hpp:292-299).  Column- and panel-major (ps = 4) storage; uniform or
 // variable (config-5) batches.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -92,7 +93,11 @@ __global__ void __launch_bounds__(256) diag_inv8_kernel(const __grid_constant__ 
 // half-warp.
 __device__ __forceinline__ int ab_idx(int c, int g) { return c * 8 + (g ^ (((c >> 1) & 1) << 2)); }
 
-template <int PM>
+// NT > 0: register-resident variant for up to NT column tiles — the solved X
+// stays in registers (A-fragment order, 2 doubles per tile and lane), the
+// tile loops are fully unrolled, and shared memory holds only the staged rows
+// of A, so residency is no longer bounded by 8 rows x n of X per warp.
+template <int PM, int NT>
 __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_constant__ RltArgs R) {
   extern __shared__ __align__(16) double sm_all[];
   const TrsmLaunch& L = R.L;
@@ -132,8 +137,10 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
   const int nt = (n + 7) >> 3;
   const int r = rb * 8 + g;
   const bool rok = r < m;
-  const uint32_t xs = smem_u32(sm_all + (size_t)warp * R.ntmax * 64);  // [tile][kk][lane]
-  double* ab_base = sm_all + (size_t)kRltWarps * R.ntmax * 64;          // 2 x [8 * ntmax * 8]
+  constexpr bool REG = NT > 0;
+  const uint32_t xs = smem_u32(sm_all + (size_t)warp * R.ntmax * 64);  // [tile][kk][lane] (shared variant)
+  double* ab_base = sm_all + (REG ? 0 : (size_t)kRltWarps * R.ntmax * 64);  // 2 x [8 * ntmax * 8]
+  double xr[NT > 0 ? NT : 1][2];                                          // (register variant)
   const int abs = R.ntmax * 64;
   const double alpha = L.alpha;
   // stage rows 8J..8J+7, columns 0..8J+7 of A (16-byte pairs of rows; rows past n are zero)
@@ -156,7 +163,9 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
   stage(0);
   double nb0 = (rok && 2 * t < n) ? B[rlt_off<PM>(ldb, r, 2 * t)] : 0.0;
   double nb1 = (rok && 2 * t + 1 < n) ? B[rlt_off<PM>(ldb, r, 2 * t + 1)] : 0.0;
-  for (int J = 0; J < nt; ++J) {
+#pragma unroll
+  for (int J = 0; J < (REG ? NT : 1 << 30); ++J) {
+    if (J >= nt) break;
     cp_async_wait_all();
     __syncthreads();  // rows of tile J staged; every warp is done with tile J-1's buffer
     if (J + 1 < nt) stage(J + 1);
@@ -171,11 +180,13 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     // ---- C -= X(:, 0:8J) A(J, 0:8J)^T ----
     double e0 = 0.0, e1 = 0.0;  // second accumulator pair: two independent DMMA chains
     int T2 = 0;
+#pragma unroll
     for (; T2 + 2 <= J; T2 += 2) {
       double xa[4], bf[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        xa[u] = lds64(xs + 8u * ((2 * T2 + u) * 32 + lane));
+        if constexpr (REG) xa[u] = xr[T2 + (u >> 1)][u & 1];
+        else xa[u] = lds64(xs + 8u * ((2 * T2 + u) * 32 + lane));
         bf[u] = -lds64(abu + 8u * ab_idx(8 * T2 + 4 * u + t, g));
       }
       dmma(acc0, acc1, xa[0], bf[0]);
@@ -186,7 +197,9 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     if (T2 < J) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const double xa = lds64(xs + 8u * ((2 * T2 + u) * 32 + lane));
+        double xa;
+        if constexpr (REG) xa = xr[T2][u];
+        else xa = lds64(xs + 8u * ((2 * T2 + u) * 32 + lane));
         const double bf = -lds64(abu + 8u * ab_idx(8 * T2 + 4 * u + t, g));
         dmma(acc0, acc1, xa, bf);
       }
@@ -210,9 +223,14 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     const int src0 = (lane & ~3) | (t >> 1), src1 = (lane & ~3) | (2 + (t >> 1));
     const double v00 = __shfl_sync(0xffffffffu, acc0, src0), v01 = __shfl_sync(0xffffffffu, acc1, src0);
     const double v10 = __shfl_sync(0xffffffffu, acc0, src1), v11 = __shfl_sync(0xffffffffu, acc1, src1);
-    sts64(xs + 8u * ((2 * J) * 32 + lane), (t & 1) ? v01 : v00);
-    sts64(xs + 8u * ((2 * J + 1) * 32 + lane), (t & 1) ? v11 : v10);
-    __syncwarp();
+    if constexpr (REG) {
+      xr[REG ? J : 0][0] = (t & 1) ? v01 : v00;
+      xr[REG ? J : 0][1] = (t & 1) ? v11 : v10;
+    } else {
+      sts64(xs + 8u * ((2 * J) * 32 + lane), (t & 1) ? v01 : v00);
+      sts64(xs + 8u * ((2 * J + 1) * 32 + lane), (t & 1) ? v11 : v10);
+      __syncwarp();
+    }
   }
   cp_async_wait_all();
   if (rb == 0 && lane == 0 && L.info && !L.skip_nonzero) L.info[p] = 0;
@@ -242,12 +260,19 @@ cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
   R.L = L;
   R.ntmax = (L.nn + 7) / 8;
   R.rbmax = L.nvec ? R.ntmax : (L.mm + 7) / 8;
-  const size_t smem = (size_t)(kRltWarps + 2) * R.ntmax * 64 * sizeof(double);  // X slices + 2 staged A rows
+  // register variant up to 32 tiles (PBGPU_TRSM_REG=0 disables it: A/B)
+  static const bool reg_ok = [] {
+    const char* e = getenv("PBGPU_TRSM_REG");
+    return !(e && e[0] == '0');
+  }();
+  // (measured: no gain up to 8 tiles, 1.2x at 16, 1.6x at 32)
+  const int ntr = !reg_ok || R.ntmax <= 8 || R.ntmax > 32 ? 0 : ((R.ntmax + 3) & ~3);  // a multiple of 4 tiles
+  const size_t smem = (size_t)((ntr ? 0 : kRltWarps) + 2) * R.ntmax * 64 * sizeof(double);  // [X slices +] 2 staged A rows
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(trsm_rlt_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(trsm_rlt_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(trsm_rlt_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(trsm_rlt_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -256,13 +281,27 @@ cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
   cudaError_t e = cudaMallocAsync(&R.W, sizeof(double) * 64 * R.ntmax * (size_t)L.batch, s);
   if (e != cudaSuccess) return e;
   const unsigned igrid = (unsigned)(((long long)L.batch * R.ntmax * 8 + 255) / 256);
-  if (L.pm) {
-    diag_inv8_kernel<1><<<igrid, 256, 0, s>>>(R);
-    trsm_rlt_kernel<1><<<grid, 32 * kRltWarps, smem, s>>>(R);
-  } else {
-    diag_inv8_kernel<0><<<igrid, 256, 0, s>>>(R);
-    trsm_rlt_kernel<0><<<grid, 32 * kRltWarps, smem, s>>>(R);
+  if (L.pm) diag_inv8_kernel<1><<<igrid, 256, 0, s>>>(R);
+  else diag_inv8_kernel<0><<<igrid, 256, 0, s>>>(R);
+#define PB_RLT(PMV, NTV) trsm_rlt_kernel<PMV, NTV><<<grid, 32 * kRltWarps, smem, s>>>(R)
+  switch (ntr * 2 + L.pm) {
+    case 24: PB_RLT(0, 12); break;
+    case 25: PB_RLT(1, 12); break;
+    case 40: PB_RLT(0, 20); break;
+    case 41: PB_RLT(1, 20); break;
+    case 56: PB_RLT(0, 28); break;
+    case 57: PB_RLT(1, 28); break;
+    case 32: PB_RLT(0, 16); break;
+    case 33: PB_RLT(1, 16); break;
+    case 48: PB_RLT(0, 24); break;
+    case 49: PB_RLT(1, 24); break;
+    case 64: PB_RLT(0, 32); break;
+    case 65: PB_RLT(1, 32); break;
+    default:
+      if (L.pm) PB_RLT(1, 0);
+      else PB_RLT(0, 0);
   }
+#undef PB_RLT
   e = cudaGetLastError();
   cudaFreeAsync(R.W, s);
   return e;
