@@ -213,7 +213,11 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
   // Right-looking blocked over 128-column panels: potrf(A11) -> A21 = A21 L11^{-T}
   // (trsm) -> A22 -= A21 A21^T (DMMA syrk) -> recurse on A22.  Problems whose
   // info turned nonzero are skipped by every later stage.
-  const int nb = 128;
+  static const int nb_env = [] {  // PBGPU_POTRF_NB: block order of the blocked path (tuning)
+    const char* e = getenv("PBGPU_POTRF_NB");
+    return e ? atoi(e) : 0;
+  }();
+  const int nb = nb_env >= 16 && nb_env <= kPotrfSmemMax && nb_env % 8 == 0 ? nb_env : 128;
   for (int c0 = 0; c0 < L.n; c0 += nb) {
     const int w = std::min(nb, L.n - c0), rest = L.n - c0 - w;
     // element (i, j) of the lower problem lives at i + j*lda (lower) or j + i*lda (upper)
