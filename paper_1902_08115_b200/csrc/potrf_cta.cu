@@ -68,8 +68,13 @@ struct PotrfCtaArgs {
   CUtensorMap tm[kCtaMaxT];
 };
 
-__host__ __device__ constexpr int cta_pstride(int T, int k) { return 8 * (T - k) + 4; }
-__host__ __device__ constexpr int cta_pbase(int T, int k) { return 64 * (k * T - k * (k - 1) / 2) + 32 * k; }
+#ifndef PB_CTA_PAD
+#define PB_CTA_PAD 4
+#endif
+__host__ __device__ constexpr int cta_pstride(int T, int k) { return 8 * (T - k) + PB_CTA_PAD; }
+__host__ __device__ constexpr int cta_pbase(int T, int k) {
+  return 64 * (k * T - k * (k - 1) / 2) + 8 * PB_CTA_PAD * k;
+}
 
 template <int PM>
 __device__ __forceinline__ long long cta_eoff(int upper, long long ld, int r, int c) {
