@@ -110,7 +110,7 @@ def test_dgemm_quick_returns_and_scale(pb):
     assert (c4 == 0.0).all()
 
 
-@pytest.mark.parametrize("s", [4, 8, 12, 28, 64, 100, 132, 320])
+@pytest.mark.parametrize("s", [4, 8, 12, 28, 36, 48, 60, 64, 72, 84, 100, 108, 132, 320])
 def test_gemm_nd_nt_batched(pb, orc, cuda, s):
     """Config 2: panel-major D = A B^T + C (non-destructive), checked per problem."""
     import torch
@@ -130,7 +130,7 @@ def test_gemm_nd_nt_batched(pb, orc, cuda, s):
         assert rel_frob(unpack(got[p], s, s), unpack(want, s, s)) <= tol(s)
 
 
-@pytest.mark.parametrize("s", [4, 8, 16, 32])
+@pytest.mark.parametrize("s", [4, 8, 16, 32, 44, 56, 76, 96])
 def test_gemm_nd_small_alpha_beta_alias(pb, orc, cuda, s):
     """Small-size branch: beta == 0 never reads C (NaN C), alpha scaling, D aliasing C."""
     import torch

@@ -30,7 +30,7 @@ if 'getrf' in what:
         roof = min(P, BW * fl / by)
         print(f"getrf n={n}: {ms:.4f} ms {fl/ms/1e9:.2f} TF roofline-frac {fl/(ms*1e-3)/roof:.3f}")
 if 'gemm_nd' in what:
-    for sz in (4, 8, 12, 16, 24, 32, 48, 64, 96, 128, 192, 256, 320):
+    for sz in ([int(x) for x in os.environ.get("SIZES", "").split(",") if x] or (4, 8, 12, 16, 24, 32, 48, 64, 96, 128, 192, 256, 320)):
         batch = (2**31) // (32 * sz * sz)
         L = sz * sz
         A = torch.rand((batch, L), device=dev, dtype=torch.float64); B = torch.rand_like(A); C = torch.rand_like(A); D = torch.empty_like(A)
