@@ -11,7 +11,13 @@
 // from the panel-major layout (fragment loads are conflict-free because a
 // 4-row panel column is 32 contiguous bytes), D overwrites C in shared memory
 // and leaves as one bulk store per chunk.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstring>
+#include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "launch.h"
@@ -314,6 +320,166 @@ static cudaError_t small_t(SmallArgs& P, cudaStream_t st) {
   const int grid = (int)std::min<long long>(P.nchunks, 2LL * num_sms());
   gemm_small_kernel<T><<<grid, 32 * SM_WARPS, smem, st>>>(P);
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Column-major NN, square packed problems (m = n = k = lda = ldb = ldc = s <= 64,
+// stride s*s): config 1's shape.  Same row-tile split as gemm_mid_kernel, one
+// problem per CTA iteration on a 2-stage ring; A, B and C arrive as ONE 2-D
+// TMA tensor copy each whose box is 4 rows taller than the problem (the rows
+// past s are the out-of-bounds zero fill), which gives the column stride
+// s + 4 = 4 mod 16 doubles: conflict-free fragment loads for both operands.
+// D is formed over C in shared memory and leaves as one tensor store.
+struct CmArgs {
+  CUtensorMap ta, tb, tc, td;
+  double alpha, beta;
+  long long batch;
+  int s;
+};
+
+template <int T>
+__global__ void __launch_bounds__(32 * T) gemm_cm_kernel(const __grid_constant__ CmArgs P) {
+  extern __shared__ __align__(1024) double sm[];
+  __shared__ __align__(8) uint64_t full[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int s = P.s, S = s + 4, ops = S * s;  // doubles per staged operand
+  const bool use_c = P.beta != 0.0;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t base = smem_u32(sm);
+  auto slot_addr = [&](int slot) { return base + 8u * (uint32_t)(slot * 3 * ops); };
+  auto tma3 = [&](uint32_t dst, const CUtensorMap* m, int prob, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(0), "r"(0), "r"(prob), "r"(smem_u32(bar))
+        : "memory");
+  };
+  auto issue = [&](long long prob, int slot) {
+    const uint32_t bytes = 8u * (uint32_t)ops;
+    const uint32_t a = slot_addr(slot);
+    mbar_arrive_expect_tx(&full[slot], use_c ? 3 * bytes : 2 * bytes);
+    tma3(a, &P.ta, (int)prob, &full[slot]);
+    tma3(a + 8u * ops, &P.tb, (int)prob, &full[slot]);
+    if (use_c) tma3(a + 16u * ops, &P.tc, (int)prob, &full[slot]);
+  };
+  int it = 0;
+  long long prob = blockIdx.x;
+  if (tid == 0 && prob < P.batch) issue(prob, 0);
+  for (; prob < P.batch; prob += gridDim.x, ++it) {
+    const int slot = it & 1;
+    const long long next = prob + gridDim.x;
+    if (tid == 0) {
+      bulk_wait_read0();  // the other slot's store (previous problem) has left shared memory
+      if (next < P.batch) issue(next, slot ^ 1);
+    }
+    mbar_wait(&full[slot], (it >> 1) & 1);
+    const uint32_t A = slot_addr(slot), B = A + 8u * ops, C = B + 8u * ops;
+    const int I = warp;
+    double acc[T][2];
+#pragma unroll
+    for (int J = 0; J < T; ++J) acc[J][0] = acc[J][1] = 0.0;
+    // rows past s are the zero fill; columns past s (s % 8 != 0) read the next operand and feed discarded outputs
+    for (int l0 = 0; l0 < s; l0 += 4) {
+      const double fa = lds64(A + 8u * ((l0 + t) * S + 8 * I + g));  // A(8I+g, l0+t)
+      double fb[T];
+#pragma unroll
+      for (int J = 0; J < T; ++J) fb[J] = lds64(B + 8u * ((8 * J + g) * S + l0 + t));  // B(l0+t, 8J+g)
+#pragma unroll
+      for (int J = 0; J < T; ++J) dmma(acc[J][0], acc[J][1], fa, fb[J]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int J = 0; J < T; ++J)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+        if (r < s && c < s) {
+          const uint32_t off = C + 8u * (c * S + r);
+          sts64(off, use_c ? fma(P.alpha, acc[J][e], P.beta * lds64(off)) : P.alpha * acc[J][e]);
+        }
+      }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                       reinterpret_cast<uint64_t>(&P.td)),
+                   "r"(0), "r"(0), "r"((int)prob), "r"(C)
+                   : "memory");
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait_read0();
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 small_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    cudaGetLastError();
+  });
+  return fn;
+}
+
+bool gemm_cm_ok(int s, const double* a, const double* b, const double* c, long long sa, long long sb,
+                long long sc, int lda, int ldb, int ldc) {
+  static const bool off = [] {
+    const char* e = getenv("PBGPU_GEMM_CM");
+    return e && e[0] == '0';
+  }();
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const long long ss = (long long)s * s;
+  return !off && s >= 32 && s <= 64 && s % 8 == 0 && lda == s && ldb == s && ldc == s && sa == ss && sb == ss &&
+         sc == ss && al(a) && al(b) && al(c) && small_encode_fn() != nullptr;
+}
+
+cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b, double beta, double* c,
+                           long long batch, cudaStream_t st) {
+  if (batch <= 0) return cudaSuccess;
+  CmArgs P;
+  memset(&P, 0, sizeof(P));
+  P.alpha = alpha; P.beta = beta; P.batch = batch; P.s = s;
+  auto enc = small_encode_fn();
+  cuuint64_t dims[3] = {(cuuint64_t)s, (cuuint64_t)s, (cuuint64_t)batch};
+  cuuint64_t strides[2] = {(cuuint64_t)s * 8, (cuuint64_t)s * s * 8};
+  cuuint32_t box[3] = {(cuuint32_t)(s + 4), (cuuint32_t)s, 1u};
+  cuuint32_t es[3] = {1, 1, 1};
+  const double* ptrs[4] = {a, b, c, c};
+  CUtensorMap* maps[4] = {&P.ta, &P.tb, &P.tc, &P.td};
+  for (int i = 0; i < 4; ++i)
+    if (enc(maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptrs[i]), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  const size_t smem = (size_t)2 * 3 * (s + 4) * s * sizeof(double);
+  const int per_sm = std::max(1, (int)((225 * 1024) / (smem + 1024)));
+  const int grid = (int)std::min<long long>(batch, (long long)per_sm * num_sms());
+#define PB_CM(TV)                                                                                        \
+  case TV: {                                                                                             \
+    static bool attr = false;                                                                            \
+    if (!attr) {                                                                                         \
+      cudaError_t e = cudaFuncSetAttribute(gemm_cm_kernel<TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           220 * 1024);                                                  \
+      if (e != cudaSuccess) return e;                                                                    \
+      attr = true;                                                                                       \
+    }                                                                                                    \
+    gemm_cm_kernel<TV><<<grid, 32 * TV, smem, st>>>(P);                                                  \
+    return cudaGetLastError();                                                                           \
+  }
+  switch (s / 8) {
+    PB_CM(4) PB_CM(5) PB_CM(6) PB_CM(7) PB_CM(8)
+  }
+#undef PB_CM
+  return cudaErrorInvalidValue;
 }
 
 bool gemm_small_ok(int s, const double* a, const double* b, const double* c, const double* d, long long sa,

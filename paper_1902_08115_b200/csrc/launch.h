@@ -55,6 +55,11 @@ bool gemm_small_ok(int s, const double* a, const double* b, const double* c, con
                    long long sb, long long sc, long long sd, int cna, int cnb, int cnc, int cnd);
 cudaError_t gemm_small_launch(int s, double alpha, const double* a, const double* b, double beta,
                               const double* c, double* d, long long batch, cudaStream_t st);
+// column-major NN square packed problems, 32 <= s <= 64, s % 8 == 0 (gemm_small.cu)
+bool gemm_cm_ok(int s, const double* a, const double* b, const double* c, long long sa, long long sb,
+                long long sc, int lda, int ldb, int ldc);
+cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b, double beta, double* c,
+                           long long batch, cudaStream_t st);
 
 }  // namespace pbg
 

@@ -350,6 +350,10 @@ static int dgemm_impl(const char* routine, bool batched, char transa, char trans
                          o.ldc = o.ldd = ldc;
                          o.vec = aligned16(p[2]) && sc % 2 == 0 && ldc % 2 == 0;
                          if (scale_only) return scale_launch(0, o, m, n, beta, 0, nb, s);
+                         // size switch (gemm.hpp:190-204): square packed NN problems up to 64
+                         if (ta == 0 && tb == 0 && m == n && n == k &&
+                             gemm_cm_ok(m, (const double*)p[0], (const double*)p[1], o.c, sa, sb, sc, lda, ldb, ldc))
+                           return gemm_cm_launch(m, alpha, (const double*)p[0], (const double*)p[1], beta, o.d, nb, s);
                          GemmLaunch g;
                          // M side: op(A)(i, l); N side: op(B)(l, j) as (x = j, l).
                          g.lay_a = ta == 0 ? L_MNC : L_KC;

@@ -57,6 +57,25 @@ def test_dgemm_cfg1_full_batch(pb, orc, cuda):
     assert err <= tol(k)
 
 
+@pytest.mark.parametrize("s", [32, 40, 48, 56, 64])
+def test_dgemm_square_nn_beta_zero_nan_c(pb, orc, cuda, s):
+    """Square packed NN branch of the size switch: beta = 0 never reads C (NaN C), alpha scaling."""
+    import torch
+    rng = np.random.default_rng(600 + s)
+    batch = 41
+    A = rng.uniform(-1, 1, (batch, s, s)); B = rng.uniform(-1, 1, (batch, s, s))
+    dA, dB = (torch.from_numpy(x.copy()).to(cuda) for x in (A, B))
+    dC = torch.full((batch, s, s), float("nan"), device=cuda, dtype=torch.float64)
+    assert pb.dgemm_batched("n", "n", s, s, s, -2.0, dA, s, s * s, dB, s, s * s, 0.0, dC, s, s * s, batch).ok()
+    got = dC.cpu().numpy()
+    assert np.isfinite(got).all()
+    for p in range(0, batch, 8):
+        want = np.zeros((s, s), order="F")
+        a_p, b_p = F(A[p].T), F(B[p].T)  # keep the operands alive across the call
+        orc.dgemm(b"n", b"n", s, s, s, -2.0, ptr(a_p), s, ptr(b_p), s, 0.0, ptr(want), s)
+        assert rel_frob(got[p].T, want) <= tol(s)
+
+
 def test_dgemm_host_pointers_single(pb, orc):
     """The netlib-shaped single call with host buffers (staged through the GPU)."""
     rng = np.random.default_rng(3)
