@@ -9,7 +9,7 @@ scaling: every rank owns its own batch; no collective on the data path).
            launching stream, max over ranks (flop model 2mnk, bench.hpp:119-138);
   e2e    — the same metric through the public API with pinned HOST buffers: every step
            copies A, B, C host->device and C back (pbgpu stages and overlaps the copies);
-  roofline — the dominant kernel (gemm_tiles_kernel) against measured HBM bandwidth:
+  roofline — the dominant kernel (gemm_cm_kernel) against measured HBM bandwidth:
            algorithmic bytes 8*(mk + kn + 2mn) per problem (SURVEY.md §8d);
   cpu_baseline — the reference's own CPU path (panelblas::dgemm compiled from
            /root/reference into oracle/_ref) on this host's cores, bounded sample;
@@ -458,11 +458,13 @@ def run_gpu_arm(args, ws, rank, local):
     if rank == 0:
         bw, peak_kind = measured_peaks()
         ach = BATCH * BYTES_PER_PROBLEM / (ms_step * 1e-3) / 1e9  # one launch per step
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+        traffic = None  # dram__bytes_read + write of this kernel per launch, from the committed ncu capture
+        tp = os.path.join(ROOT, "profiles", "r01_ncu_kernels.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                kd = json.load(f).get("dgemm64", {})
+            if kd.get("dram_bytes_read") is not None and kd.get("dram_bytes_write") is not None:
+                traffic = kd["dram_bytes_read"] + kd["dram_bytes_write"]
         dmma = pb.lib().pb_probe_dmma_tflops()
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
@@ -472,7 +474,7 @@ def run_gpu_arm(args, ws, rank, local):
                 "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": bw, "unit": "GB/s",
                              "frac": round(ach / bw, 4), "traffic": traffic,
                              "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
-                             "kernel": "gemm_tiles_kernel<L_MNC,L_KC,0>",
+                             "kernel": "gemm_cm_kernel<8> (square packed NN branch of the size switch)",
                              "algorithmic_bytes_per_launch": BATCH * BYTES_PER_PROBLEM,
                              "fp64_roofline_gflops": round(min(dmma * 1e3, bw * 4.0), 1),
                              "fp64_frac": round(value / ws / min(dmma * 1e3, bw * 4.0), 4),

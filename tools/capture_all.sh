@@ -9,4 +9,4 @@ bash tools/launch_list.sh getrf192 getrf 192 1
 bash tools/launch_list.sh potrf256 potrf 256 1
 bash tools/prof1.sh "potrf32 potrf_reg potrf 32 2" "potrf64 potrf_cta potrf 64 2" "potrf128 potrf_cta potrf 128 2" \
   "getrf24 getrf_reg getrf 24 2" "getrf48 getrf_cta getrf 48 2" "trsm256 trsm_rlt trsm 256 2" \
-  "gemmnd4 gemm gemm_nd 4 2" "gemmnd96 gemm gemm_nd 96 2"
+  "gemmnd4 gemm gemm_nd 4 2" "gemmnd48 gemm gemm_nd 48 2" "gemmnd96 gemm gemm_nd 96 2" "dgemm64 gemm gemm 64 3"
