@@ -215,6 +215,19 @@ __global__ void __launch_bounds__(32 * T) gemm_mid_kernel(const __grid_constant_
     const double* B = A + ss;
     double* Cq = bufp(slot) + 2 * ss;
     const int I = warp;
+    const double* Cg = P.c + prob * ss;
+    double* Dg = P.d + prob * ss;
+    double cpre[SC ? 1 : T][2];  // unstaged C: loaded before the k loop so its latency hides under it
+    if constexpr (!SC) {
+#pragma unroll
+      for (int J = 0; J < T; ++J)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+          const long long off = (long long)(r >> 2) * 4 * s + c * 4 + (r & 3);
+          cpre[J][e] = ldg_if(Cg + off, use_c && r < s && c < s, 0.0);
+        }
+    }
     double acc[T][2];
 #pragma unroll
     for (int J = 0; J < T; ++J) acc[J][0] = acc[J][1] = 0.0;
@@ -237,8 +250,6 @@ __global__ void __launch_bounds__(32 * T) gemm_mid_kernel(const __grid_constant_
     } else {
       __syncwarp();
     }
-    const double* Cg = P.c + prob * ss;
-    double* Dg = P.d + prob * ss;
 #pragma unroll
     for (int J = 0; J < T; ++J)
 #pragma unroll
@@ -246,8 +257,8 @@ __global__ void __launch_bounds__(32 * T) gemm_mid_kernel(const __grid_constant_
         const int r = 8 * I + g, c = 8 * J + 2 * t + e;
         if (r < s && c < s) {
           const long long off = (long long)(r >> 2) * 4 * s + c * 4 + (r & 3);
-          if (SC) Cq[off] = use_c ? fma(P.alpha, acc[J][e], P.beta * Cq[off]) : P.alpha * acc[J][e];
-          else Dg[off] = use_c ? fma(P.alpha, acc[J][e], P.beta * Cg[off]) : P.alpha * acc[J][e];
+          if constexpr (SC) Cq[off] = use_c ? fma(P.alpha, acc[J][e], P.beta * Cq[off]) : P.alpha * acc[J][e];
+          else Dg[off] = use_c ? fma(P.alpha, acc[J][e], P.beta * cpre[J][e]) : P.alpha * acc[J][e];
         }
       }
     if (SC) {
@@ -488,9 +499,9 @@ bool gemm_small_ok(int s, const double* a, const double* b, const double* c, con
   const long long ss = (long long)s * s;
   static const int mid_hi = [] {  // PBGPU_GEMM_MID_HI: largest order on gemm_mid_kernel (tuning)
     const char* e = getenv("PBGPU_GEMM_MID_HI");
-    return e ? atoi(e) : 104;  // measured: the engine is ahead from s = 108
+    return e ? atoi(e) : 112;
   }();
-  return s > 0 && s <= std::min(mid_hi, 108) && s % 4 == 0 && sa == ss && sb == ss && sc == ss && sd == ss && cna == s &&
+  return s > 0 && s <= std::min(mid_hi, 112) && s % 4 == 0 && sa == ss && sb == ss && sc == ss && sd == ss && cna == s &&
          cnb == s && cnc == s && cnd == s && al(a) && al(b) && al(c) && al(d);
 }
 
