@@ -161,8 +161,13 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     }
   };
   stage(0);
-  double nb0 = (rok && 2 * t < n) ? B[rlt_off<PM>(ldb, r, 2 * t)] : 0.0;
-  double nb1 = (rok && 2 * t + 1 < n) ? B[rlt_off<PM>(ldb, r, 2 * t + 1)] : 0.0;
+  // X(r, c) of the effective problem: B / D element (r, c), or (c, r) for a Left
+  // solve run as its transposed twin (level3.hpp:300-303; column-major only)
+  auto xo = [&](long long ld, int rr, int cc) -> long long {
+    return (!PM && L.twin) ? (long long)cc + (long long)rr * ld : rlt_off<PM>(ld, rr, cc);
+  };
+  double nb0 = (rok && 2 * t < n) ? B[xo(ldb, r, 2 * t)] : 0.0;
+  double nb1 = (rok && 2 * t + 1 < n) ? B[xo(ldb, r, 2 * t + 1)] : 0.0;
 #pragma unroll
   for (int J = 0; J < (REG ? NT : 1 << 30); ++J) {
     if (J >= nt) break;
@@ -174,8 +179,8 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     const int ca = 8 * J + 2 * t, cb = ca + 1;
     double acc0 = alpha * nb0, acc1 = alpha * nb1;
     if (J + 1 < nt) {  // next tile's right-hand side, loaded under this tile's work
-      nb0 = (rok && ca + 8 < n) ? B[rlt_off<PM>(ldb, r, ca + 8)] : 0.0;
-      nb1 = (rok && cb + 8 < n) ? B[rlt_off<PM>(ldb, r, cb + 8)] : 0.0;
+      nb0 = (rok && ca + 8 < n) ? B[xo(ldb, r, ca + 8)] : 0.0;
+      nb1 = (rok && cb + 8 < n) ? B[xo(ldb, r, cb + 8)] : 0.0;
     }
     // ---- C -= X(:, 0:8J) A(J, 0:8J)^T ----
     double e0 = 0.0, e1 = 0.0;  // second accumulator pair: two independent DMMA chains
@@ -217,8 +222,8 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
       dmma(acc0, acc1, (t & 1) ? u01 : u00, w0);
       dmma(acc0, acc1, (t & 1) ? u11 : u10, w1);
     }
-    if (rok && ca < n) D[rlt_off<PM>(ldd, r, ca)] = acc0;
-    if (rok && cb < n) D[rlt_off<PM>(ldd, r, cb)] = acc1;
+    if (rok && ca < n) D[xo(ldd, r, ca)] = acc0;
+    if (rok && cb < n) D[xo(ldd, r, cb)] = acc1;
     // ---- re-lay as A fragments: kk = 0 needs column t, kk = 1 column 4 + t ----
     const int src0 = (lane & ~3) | (t >> 1), src1 = (lane & ~3) | (2 + (t >> 1));
     const double v00 = __shfl_sync(0xffffffffu, acc0, src0), v01 = __shfl_sync(0xffffffffu, acc1, src0);
@@ -252,7 +257,7 @@ void mempool_keep() {
   done_dev = dev;
 }
 
-bool trsm_rlt_ok(const TrsmLaunch& L) { return !L.twin && L.lower && L.trans && L.nn <= 512; }
+bool trsm_rlt_ok(const TrsmLaunch& L) { return !(L.twin && L.pm) && L.lower && L.trans && L.nn <= 512; }
 
 cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.mm <= 0 || L.nn <= 0) return cudaSuccess;
