@@ -492,7 +492,16 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
 #ifdef PB_PANEL_REDUNDANT
       const int f = cta_factor_panel<R>(sbase + 8u * cta_pbase(T, k), RS, rows, lane, 8 * k, n);
 #else
-      const int f = cta_factor_panel_bc<R>(sbase + 8u * cta_pbase(T, k), RS, rows, lane, 8 * k, n, smem_u32(&sh_col[0][0]));
+      // rows per lane follow the panel's height (fewer predicated-off rows in late panels)
+      const uint32_t pk = sbase + 8u * cta_pbase(T, k), cbuf = smem_u32(&sh_col[0][0]);
+      int f;
+      if constexpr (R > 1) {
+        if (rows <= 32) f = cta_factor_panel_bc<1>(pk, RS, rows, lane, 8 * k, n, cbuf);
+        else if (R > 2 && rows <= 64) f = cta_factor_panel_bc<(R > 2 ? 2 : R)>(pk, RS, rows, lane, 8 * k, n, cbuf);
+        else f = cta_factor_panel_bc<R>(pk, RS, rows, lane, 8 * k, n, cbuf);
+      } else {
+        f = cta_factor_panel_bc<R>(pk, RS, rows, lane, 8 * k, n, cbuf);
+      }
 #endif
       if (f && lane == 0) sh_fail = 8 * k + f;
       if (lane == 0) { PB_STAMP(5 + 2 * k) }
@@ -523,8 +532,8 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
     }
     if (!fail) named_sync(1, NTH);  // the last panel's publication
   }
-  if (streamed || P.tma)  // a failure can stop before late panels land: no async copy may outlive the CTA
-    for (int k = 0; k < TT; ++k) mbar_wait(&sh_bar[k], 0);
+  if ((streamed || P.tma) && sh_fail)  // a failure can stop before late panels land: no async copy may
+    for (int k = 0; k < TT; ++k) mbar_wait(&sh_bar[k], 0);  // outlive the CTA (without one, all were consumed)
   __syncthreads();
   fail = sh_fail;
   if (tid == 0) { PB_STAMP(2) }
