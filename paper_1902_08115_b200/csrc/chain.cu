@@ -207,18 +207,21 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
   for (auto& kv : big) {
     const int n = kv.first, cnt = (int)kv.second.size();
     const long long nn = (long long)n * n;  // n % 4 == 0 in panel-major: pm = cn = n
-    double *wa = nullptr, *wc = nullptr, *wb = nullptr;
+    double *wa = nullptr, *wc = nullptr;
     int *d_i = nullptr, *w_info = nullptr;
-    if ((e = cudaMallocAsync(&wa, sizeof(double) * nn * cnt * 3, s)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&wa, sizeof(double) * nn * cnt * 2, s)) != cudaSuccess) return e;
     wc = wa + nn * cnt;
-    wb = wc + nn * cnt;
+    long long* d_ob = nullptr;  // B stays in place: the solve reads and writes it at its own offsets
     cudaMallocAsync(&d_i, sizeof(int) * cnt, s);
     cudaMallocAsync(&w_info, sizeof(int) * cnt, s);
+    cudaMallocAsync(&d_ob, sizeof(long long) * cnt, s);
+    std::vector<long long> ob(cnt);
+    for (int q = 0; q < cnt; ++q) ob[q] = ov[kv.second[q]];
     cudaMemcpyAsync(d_i, kv.second.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_ob, ob.data(), sizeof(long long) * cnt, cudaMemcpyHostToDevice, s);
     dim3 gg = grid2(nn, cnt);
     gather_kernel<<<gg, 256, 0, s>>>(L.A, L.offset, d_i, wa, (int)nn);
     gather_kernel<<<gg, 256, 0, s>>>(L.C, L.offset, d_i, wc, (int)nn);
-    gather_kernel<<<gg, 256, 0, s>>>(L.B, L.offset, d_i, wb, (int)nn);
     if (!L.pm) {
       GemmLaunch g;  // dsyrk('l','n'): C += A A^T
       g.lay_a = g.lay_b = L_MNC;
@@ -249,8 +252,9 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       T.mm = T.nn = n;
       T.alpha = 1.0;
       T.a = wc; T.sa = nn; T.lda = n;
-      T.b = wb; T.sb = nn; T.ldb = n;
-      T.d = wb; T.sd = nn; T.ldd = n;
+      T.b = L.B; T.ldb = n;
+      T.d = L.B; T.ldd = n;
+      T.offs_b = d_ob;
       T.info = w_info;
       T.skip_nonzero = 1;
       T.batch = cnt;
@@ -258,12 +262,12 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
     }
     if (e == cudaSuccess) {
       scatter_kernel<<<gg, 256, 0, s>>>(wc, L.C, L.offset, d_i, (int)nn);
-      scatter_kernel<<<gg, 256, 0, s>>>(wb, L.B, L.offset, d_i, (int)nn);
       scatter_info_kernel<<<std::max(1, (cnt + 255) / 256), 256, 0, s>>>(w_info, d_i, L.info, cnt);
       e = cudaGetLastError();
     }
     cudaFreeAsync(wa, s);
     cudaFreeAsync(d_i, s);
+    cudaFreeAsync(d_ob, s);
     cudaFreeAsync(w_info, s);
     if (e != cudaSuccess) return e;
   }

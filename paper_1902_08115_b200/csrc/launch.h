@@ -159,6 +159,9 @@ struct TrsmLaunch {
   // round_up(n, 4)) and element offsets shared by a, b and d
   const int* nvec = nullptr;
   const long long* offs = nullptr;
+  // optional: uniform strided a (sa) with b / d at per-problem element offsets
+  // (the chain's large orders: the factor in a gathered workspace, B in place)
+  const long long* offs_b = nullptr;
 };
 cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s);
 // warp-per-8-rows left-looking DMMA solve for X * A^T = alpha B, A lower (trsm_rlt.cu);

@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     D = L.d + L.offs[p];
   } else {
     A = L.a + p * L.sa;
-    B = L.b + p * L.sb;
-    D = L.d + p * L.sd;
+    B = L.b + (L.offs_b ? L.offs_b[p] : p * L.sb);
+    D = L.d + (L.offs_b ? L.offs_b[p] : p * L.sd);
   }
   if ((rb - warp) * 8 >= m) return;  // CTA-uniform: no row of this CTA exists
   // ---- zero diagonal: smallest exactly-zero index, before any store ----
@@ -258,6 +258,7 @@ void mempool_keep() {
 }
 
 bool trsm_rlt_ok(const TrsmLaunch& L) { return !(L.twin && L.pm) && L.lower && L.trans && L.nn <= 512; }
+// (offs_b is honoured only here: trsm_launch forwards every such launch to this kernel)
 
 cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.mm <= 0 || L.nn <= 0) return cudaSuccess;
