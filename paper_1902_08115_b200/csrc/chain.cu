@@ -157,10 +157,11 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       so[q] = ov[small[q]];
       sn[q] = nv[small[q]];
     }
-    if ((e = cudaMallocAsync(&d_idx, sizeof(int) * nsm, s)) != cudaSuccess) return e;
-    cudaMallocAsync(&d_n, sizeof(int) * nsm, s);
-    cudaMallocAsync(&d_info, sizeof(int) * nsm, s);
-    cudaMallocAsync(&d_off, sizeof(long long) * nsm, s);
+    if ((e = cudaMallocAsync(&d_idx, sizeof(int) * nsm, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&d_n, sizeof(int) * nsm, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&d_info, sizeof(int) * nsm, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&d_off, sizeof(long long) * nsm, s)) != cudaSuccess)
+      return e;
     cudaMemcpyAsync(d_idx, small.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_n, sn.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_off, so.data(), sizeof(long long) * nsm, cudaMemcpyHostToDevice, s);
@@ -209,12 +210,13 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
     const long long nn = (long long)n * n;  // n % 4 == 0 in panel-major: pm = cn = n
     double *wa = nullptr, *wc = nullptr;
     int *d_i = nullptr, *w_info = nullptr;
-    if ((e = cudaMallocAsync(&wa, sizeof(double) * nn * cnt * 2, s)) != cudaSuccess) return e;
-    wc = wa + nn * cnt;
     long long* d_ob = nullptr;  // B stays in place: the solve reads and writes it at its own offsets
-    cudaMallocAsync(&d_i, sizeof(int) * cnt, s);
-    cudaMallocAsync(&w_info, sizeof(int) * cnt, s);
-    cudaMallocAsync(&d_ob, sizeof(long long) * cnt, s);
+    if ((e = cudaMallocAsync(&wa, sizeof(double) * nn * cnt * 2, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&d_i, sizeof(int) * cnt, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&w_info, sizeof(int) * cnt, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&d_ob, sizeof(long long) * cnt, s)) != cudaSuccess)
+      return e;
+    wc = wa + nn * cnt;
     std::vector<long long> ob(cnt);
     for (int q = 0; q < cnt; ++q) ob[q] = ov[kv.second[q]];
     cudaMemcpyAsync(d_i, kv.second.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, s);
