@@ -42,7 +42,7 @@ constexpr int kRegWarps = 4;
 // CS != 0: compile-time column stride (packed column-major lower problems,
 // lda == n == N): every access is the row pointer plus an immediate offset.
 template <int N, int W, int PM, int CS>
-__global__ void __launch_bounds__(32 * kRegWarps, 4) potrf_reg_kernel(const __grid_constant__ PotrfRegArgs P) {
+__global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_kernel(const __grid_constant__ PotrfRegArgs P) {
   static_assert(N <= W && W <= 32 && 32 % W == 0, "segment shape");
   constexpr int SEGS = 32 / W;
   __shared__ __align__(16) double colbuf[kRegWarps][2][32];
