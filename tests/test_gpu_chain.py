@@ -108,3 +108,47 @@ def test_chain_vbatched(pb, orc, cuda, layout):
             assert orc.trsm_rltn_nd(n, n, 1.0, dmat(c, n, n), dmat(b, n, n), dmat(b, n, n)) == 0
             assert rel_frob(gC[o:o + n * n], c) <= tol(n)
             assert rel_frob(gB[o:o + n * n], b) <= tol(n) * 10
+
+
+def test_chain_cfg5_full_batch_properties(pb, cuda):
+    """Config 5 at full size (32768 problems, n = 4 U{1..64}, column-major): every problem
+    checked on the device by size-independent properties — the factor reproduces
+    C0 + A A^T (||L L^T - S|| / ||S||) and the solve satisfies ||X L^T - B|| / ||B|| —
+    within the north star's 1e-13 n."""
+    import torch
+    rng = np.random.default_rng(55)
+    batch = 32768
+    ns = rng.integers(1, 65, batch) * 4
+    offs = np.concatenate([[0], np.cumsum(ns.astype(np.int64) ** 2)[:-1]])
+    total = int((ns.astype(np.int64) ** 2).sum())
+    g = torch.Generator(device=cuda).manual_seed(55)
+    A = torch.rand(total, generator=g, device=cuda, dtype=torch.float64) * 2 - 1
+    B0 = torch.rand(total, generator=g, device=cuda, dtype=torch.float64) * 2 - 1
+    C = torch.zeros(total, device=cuda, dtype=torch.float64)
+    for n in np.unique(ns):
+        idx = np.nonzero(ns == n)[0]
+        base = torch.from_numpy(offs[idx]).to(cuda)
+        ar = torch.arange(int(n), device=cuda)
+        C[(base[:, None] + (ar * (int(n) + 1))[None, :]).reshape(-1)] = float(n)
+    B = B0.clone()
+    dn = torch.from_numpy(ns.astype(np.int32)).to(cuda)
+    doff = torch.from_numpy(offs).to(cuda)
+    info = torch.full((batch,), -9, dtype=torch.int32, device=cuda)
+    assert pb.chain_vbatched("C", dn, doff, A, C, B, info, batch, 256).ok()
+    torch.cuda.synchronize()
+    assert int(info.abs().sum()) == 0
+    worst = 0.0
+    for n in np.unique(ns):
+        n = int(n)
+        idx = torch.from_numpy(offs[ns == n]).to(cuda)
+        gidx = (idx[:, None] + torch.arange(n * n, device=cuda)[None, :])
+        # column-major n x n blocks: element (i, j) at i + j n -> view as (batch, j, i), transpose
+        a = A[gidx].view(-1, n, n).transpose(1, 2)
+        l = torch.tril(C[gidx].view(-1, n, n).transpose(1, 2))
+        x = B[gidx].view(-1, n, n).transpose(1, 2)
+        b = B0[gidx].view(-1, n, n).transpose(1, 2)
+        s = a @ a.transpose(1, 2) + n * torch.eye(n, device=cuda, dtype=torch.float64)
+        e1 = (torch.linalg.matrix_norm(l @ l.transpose(1, 2) - s) / torch.linalg.matrix_norm(s)).max().item()
+        e2 = (torch.linalg.matrix_norm(x @ l.transpose(1, 2) - b) / torch.linalg.matrix_norm(b)).max().item()
+        worst = max(worst, e1 / tol(n), e2 / tol(n))
+    assert worst <= 1.0, worst

@@ -227,3 +227,26 @@ def test_syrk_nd(pb, orc):
         orc.syrk_nd(n, k, 1.0, dmat(ap, n, k), 1.0, dmat(cp, n, n), dmat(want, n, n))
         assert rel_frob(unpack(d, n, n), unpack(want, n, n)) <= tol(k)
         assert rel_frob(d, want) <= tol(k)  # includes the untouched upper part
+
+
+@pytest.mark.parametrize("s", [4, 48, 96])
+def test_gemm_nd_cfg2_full_batch(pb, cuda, s):
+    """Config 2 at full size (batch = 2^31 / (32 s^2)) on the size-switched kernels: every problem
+    checked against torch fp64 through the panel-major layout (element (i, j) at (i/4)*4s + 4j + i%4)."""
+    import torch
+    batch = (2 ** 31) // (32 * s * s)
+    L = s * s
+    g = torch.Generator(device=cuda).manual_seed(s)
+    A = torch.rand((batch, L), generator=g, device=cuda, dtype=torch.float64) * 2 - 1
+    B = torch.rand((batch, L), generator=g, device=cuda, dtype=torch.float64) * 2 - 1
+    C = torch.rand((batch, L), generator=g, device=cuda, dtype=torch.float64) * 2 - 1
+    D = torch.empty_like(A)
+    R = pb.PanelRef
+    assert pb.gemm_nd_batched("n", "t", s, s, s, 1.0, R(A, s, s), L, R(B, s, s), L, 1.0, R(C, s, s), L,
+                              R(D, s, s), L, batch).ok()
+
+    def dense(x):  # (batch, s/4 panels, s cols, 4 rows) -> (batch, s rows, s cols)
+        return x.view(batch, s // 4, s, 4).permute(0, 1, 3, 2).reshape(batch, s, s)
+    want = dense(A) @ dense(B).transpose(1, 2) + dense(C)
+    err = (torch.linalg.matrix_norm(dense(D) - want) / torch.linalg.matrix_norm(want)).max().item()
+    assert err <= tol(s)
