@@ -41,45 +41,56 @@ constexpr int kRegWarps = 4;
 
 // CS != 0: compile-time column stride (packed column-major lower problems,
 // lda == n == N): every access is the row pointer plus an immediate offset.
-template <int N, int W, int PM, int CS>
+template <int N, int W, int PM, int CS, int RR>
 __global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_kernel(const __grid_constant__ PotrfRegArgs P) {
-  static_assert(N <= W && W <= 32 && 32 % W == 0, "segment shape");
+  // RR rows per lane: lane i of a W-lane segment owns rows i, i + W, ... (N <= W * RR)
+  static_assert(N <= W * RR && W <= 32 && 32 % W == 0, "segment shape");
   constexpr int SEGS = 32 / W;
-  __shared__ __align__(16) double colbuf[kRegWarps][2][32];
+  __shared__ __align__(16) double colbuf[kRegWarps][2][32 * RR];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = lane % W, sbase = lane - i;  // row, first lane of the segment
-  const long long p = ((long long)blockIdx.x * kRegWarps + warp) * SEGS + lane / W;
+  const int i = lane % W, seg = lane / W;
+  const long long p = ((long long)blockIdx.x * kRegWarps + warp) * SEGS + seg;
   const bool live = p < P.batch && !(P.skip_nonzero && P.info[p] != 0);
   const int n = live ? (P.nvec ? P.nvec[p] : P.n) : 0;
   double* a = P.a + (live ? (P.offs ? P.offs[p] : p * P.stride) : 0);
   const long long lda = CS ? CS : (P.nvec ? (PM ? ((n + 3) & ~3) : n) : P.lda);
-
-  // element (i, j) of the lower problem is rp[j * cs] in all three storage kinds
-  double* rp = a + (PM ? (long long)(i >> 2) * 4 * lda + (i & 3) : ((!CS && P.upper) ? (long long)i * lda : i));
   const long long cs = CS ? CS : (PM ? 4 : (P.upper ? 1 : lda));
-  double x[N];
+  // element (r, j) of the lower problem is rowp(r)[j * cs] in all three storage kinds
+  auto rowp = [&](int r) -> double* {
+    return a + (PM ? (long long)(r >> 2) * 4 * lda + (r & 3) : ((!CS && P.upper) ? (long long)r * lda : r));
+  };
+  double x[RR][N];
 #pragma unroll
-  for (int j = 0; j < N; ++j) x[j] = ldg_if(rp + j * cs, j <= i && i < n, i == j ? 1.0 : 0.0);
+  for (int q = 0; q < RR; ++q) {
+    const int r = i + W * q;
+    double* rp = rowp(r);
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[q][j] = ldg_if(rp + j * cs, j <= r && r < n, r == j ? 1.0 : 0.0);
+  }
 
-  const uint32_t buf0 = smem_u32(&colbuf[warp][0][sbase]);
+  const uint32_t buf0 = smem_u32(&colbuf[warp][0][seg * W * RR]);
   unsigned bad = 0;  // bit c: column c's pivot failed the test
 #pragma unroll
   for (int c = 0; c < N; ++c) {
-    const uint32_t buf = buf0 + (c & 1) * 32 * 8;
-    sts64(buf + 8u * i, x[c]);
+    const uint32_t buf = buf0 + (c & 1) * 32 * RR * 8;
+#pragma unroll
+    for (int q = 0; q < RR; ++q) sts64(buf + 8u * (i + W * q), x[q][c]);
     __syncwarp();
     double col[N];
 #pragma unroll
     for (int c2 = c & ~1; c2 < N; c2 += 2) lds128(buf + 8u * c2, col[c2], col[c2 + 1]);
-    const double piv = col[c];  // == x[c] on lane c
+    const double piv = col[c];  // == x[.][c] on the row c
     bad |= (piv <= 0.0 ? 1u : 0u) << c;
     double inv = rsqrt_nb(piv);
     if (__any_sync(0xffffffffu, rsqrt_special(piv)))  // denormal / +inf pivots: exact path
       inv = rsqrt_special(piv) ? rsqrt(piv) : inv;
-    x[c] *= inv;
-    const double t = x[c] * inv;
 #pragma unroll
-    for (int c2 = c + 1; c2 < N; ++c2) x[c2] = fma(-t, col[c2], x[c2]);
+    for (int q = 0; q < RR; ++q) {
+      x[q][c] *= inv;
+      const double t = x[q][c] * inv;
+#pragma unroll
+      for (int c2 = c + 1; c2 < N; ++c2) x[q][c2] = fma(-t, col[c2], x[q][c2]);
+    }
   }
   const unsigned nmask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);
   const int fail = __ffs(bad & nmask);  // first failing column, 1-based (0: none)
@@ -91,18 +102,22 @@ __global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_k
       band_lo = ((fail - 1) / 8) * 8 + 8;
       ncols = ((fail - 1) / 4) * 4;
     }
-    const bool row_ok = i < n && i < band_lo;
-    if (CS) {
 #pragma unroll
-      for (int j = 0; j < N; ++j) stg_if(rp + j * CS, x[j], row_ok && j <= i && j < ncols);
-    } else {
-      double* wp = rp;
+    for (int q = 0; q < RR; ++q) {
+      const int r = i + W * q;
+      const bool row_ok = r < n && r < band_lo;
+      double* wp = rowp(r);
+      if (CS) {
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        const bool lower = j <= i;
-        const bool zero = P.zero_fill && i < j && (i >> 3) == (j >> 3);
-        stg_if(wp, lower ? x[j] : 0.0, row_ok && j < ncols && (lower || zero));
-        wp += cs;
+        for (int j = 0; j < N; ++j) stg_if(wp + j * CS, x[q][j], row_ok && j <= r && j < ncols);
+      } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const bool lower = j <= r;
+          const bool zero = P.zero_fill && r < j && (r >> 3) == (j >> 3);
+          stg_if(wp, lower ? x[q][j] : 0.0, row_ok && j < ncols && (lower || zero));
+          wp += cs;
+        }
       }
     }
     if (i == 0) P.info[p] = fail ? fail + P.info_offset : 0;
@@ -111,17 +126,17 @@ __global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_k
   }
 }
 
-template <int N, int W, int PM>
+template <int N, int W, int PM, int RR = 1>
 static cudaError_t reg_launch_t(const PotrfRegArgs& P, cudaStream_t s) {
   constexpr int per_cta = kRegWarps * (32 / W);
   const unsigned grid = (unsigned)((P.batch + per_cta - 1) / per_cta);
   if constexpr (!PM) {
     if (!P.upper && !P.nvec && !P.offs && !P.zero_fill && P.n == N && P.lda == N) {
-      potrf_reg_kernel<N, W, 0, N><<<grid, 32 * kRegWarps, 0, s>>>(P);
+      potrf_reg_kernel<N, W, 0, N, RR><<<grid, 32 * kRegWarps, 0, s>>>(P);
       return cudaGetLastError();
     }
   }
-  potrf_reg_kernel<N, W, PM, 0><<<grid, 32 * kRegWarps, 0, s>>>(P);
+  potrf_reg_kernel<N, W, PM, 0, RR><<<grid, 32 * kRegWarps, 0, s>>>(P);
   return cudaGetLastError();
 }
 
@@ -130,7 +145,7 @@ static cudaError_t reg_dispatch(const PotrfRegArgs& P, int nmax, cudaStream_t s)
   if (nmax <= 4) return reg_launch_t<4, 8, PM>(P, s);
   if (nmax <= 8) return reg_launch_t<8, 8, PM>(P, s);
   if (nmax <= 12) return reg_launch_t<12, 16, PM>(P, s);
-  if (nmax <= 16) return reg_launch_t<16, 16, PM>(P, s);
+  if (nmax <= 16) return reg_launch_t<16, 8, PM, 2>(P, s);  // two rows per lane, four problems per warp
   if (nmax <= 24) return reg_launch_t<24, 32, PM>(P, s);
   if (nmax <= 32) return reg_launch_t<32, 32, PM>(P, s);
   return cudaErrorInvalidValue;
