@@ -206,9 +206,13 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
   }();
   if (kernel == 1 && L.n <= 64)
     return potrf_warp_launch(L.a, L.stride, L.lda, L.n, L.upper, L.info, 0, 0, L.batch, s);
-  if (kernel == 0 && L.n <= kPotrfSmemMax)
+  static const int blocked_from = [] {  // PBGPU_POTRF_BLOCKED_FROM=n: blocked path from this order on (tuning)
+    const char* e = getenv("PBGPU_POTRF_BLOCKED_FROM");
+    return e ? atoi(e) : kPotrfSmemMax + 1;
+  }();
+  if (kernel == 0 && L.n <= kPotrfSmemMax && L.n < blocked_from)
     return potrf_cta_launch(L.a, L.stride, nullptr, nullptr, L.lda, L.n, L.upper, 0, 0, L.info, 0, 0, L.batch, s);
-  if (L.n <= kPotrfSmemMax)
+  if (L.n <= kPotrfSmemMax && L.n < blocked_from)
     return potrf_smem(L.a, L.stride, L.lda, L.n, L.upper, L.info, 0, 0, L.batch, s);
   // Right-looking blocked over 128-column panels: potrf(A11) -> A21 = A21 L11^{-T}
   // (trsm) -> A22 -= A21 A21^T (DMMA syrk) -> recurse on A22.  Problems whose
