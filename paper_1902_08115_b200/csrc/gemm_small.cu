@@ -341,6 +341,9 @@ static cudaError_t small_t(SmallArgs& P, cudaStream_t st) {
 // past s are the out-of-bounds zero fill), which gives the column stride
 // s + 4 = 4 mod 16 doubles: conflict-free fragment loads for both operands.
 // D is formed over C in shared memory and leaves as one tensor store.
+#ifndef CM_PAD
+#define CM_PAD 4  // box rows past s (out-of-bounds zero fill): column stride s + 4 = 4 mod 16
+#endif
 struct CmArgs {
   CUtensorMap ta, tb, tc, td;
   double alpha, beta;
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(32 * T) gemm_cm_kernel(const __grid_constant__
   extern __shared__ __align__(1024) double sm[];
   __shared__ __align__(8) uint64_t full[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int s = P.s, S = s + 4, ops = S * s;  // doubles per staged operand
+  const int s = P.s, S = s + CM_PAD, ops = S * s;  // doubles per staged operand
   const bool use_c = P.beta != 0.0;
   if (tid == 0) {
     mbar_init(&full[0], 1);
@@ -462,7 +465,7 @@ cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b
   auto enc = small_encode_fn();
   cuuint64_t dims[3] = {(cuuint64_t)s, (cuuint64_t)s, (cuuint64_t)batch};
   cuuint64_t strides[2] = {(cuuint64_t)s * 8, (cuuint64_t)s * s * 8};
-  cuuint32_t box[3] = {(cuuint32_t)(s + 4), (cuuint32_t)s, 1u};
+  cuuint32_t box[3] = {(cuuint32_t)(s + CM_PAD), (cuuint32_t)s, 1u};
   cuuint32_t es[3] = {1, 1, 1};
   const double* ptrs[4] = {a, b, c, c};
   CUtensorMap* maps[4] = {&P.ta, &P.tb, &P.tc, &P.td};
@@ -471,7 +474,7 @@ cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
-  const size_t smem = (size_t)2 * 3 * (s + 4) * s * sizeof(double);
+  const size_t smem = (size_t)2 * 3 * (s + CM_PAD) * s * sizeof(double);
   const int per_sm = std::max(1, (int)((225 * 1024) / (smem + 1024)));
   const int grid = (int)std::min<long long>(batch, (long long)per_sm * num_sms());
 #define PB_CM(TV)                                                                                        \
