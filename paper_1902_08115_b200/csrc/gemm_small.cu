@@ -351,8 +351,11 @@ struct CmArgs {
   int s;
 };
 
+#ifndef CM_SPLIT
+#define CM_SPLIT 2
+#endif
 template <int T>
-__global__ void __launch_bounds__(32 * T) gemm_cm_kernel(const __grid_constant__ CmArgs P) {
+__global__ void __launch_bounds__(32 * T * CM_SPLIT) gemm_cm_kernel(const __grid_constant__ CmArgs P) {
   extern __shared__ __align__(1024) double sm[];
   __shared__ __align__(8) uint64_t full[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -393,26 +396,31 @@ __global__ void __launch_bounds__(32 * T) gemm_cm_kernel(const __grid_constant__
     }
     mbar_wait(&full[slot], (it >> 1) & 1);
     const uint32_t A = slot_addr(slot), B = A + 8u * ops, C = B + 8u * ops;
-    const int I = warp;
-    double acc[T][2];
+    // CM_SPLIT warps per row tile, each owning T / CM_SPLIT column tiles
+    constexpr int TJ = (T + CM_SPLIT - 1) / CM_SPLIT;
+    const int I = warp % T, J0 = (warp / T) * TJ;
+    const int nj = min(TJ, T - J0);  // warp-uniform (odd T: the last split owns fewer tiles)
+    double acc[TJ][2];
 #pragma unroll
-    for (int J = 0; J < T; ++J) acc[J][0] = acc[J][1] = 0.0;
+    for (int J = 0; J < TJ; ++J) acc[J][0] = acc[J][1] = 0.0;
     // rows past s are the zero fill; columns past s (s % 8 != 0) read the next operand and feed discarded outputs
     for (int l0 = 0; l0 < s; l0 += 4) {
       const double fa = lds64(A + 8u * ((l0 + t) * S + 8 * I + g));  // A(8I+g, l0+t)
-      double fb[T];
+      double fb[TJ];
 #pragma unroll
-      for (int J = 0; J < T; ++J) fb[J] = lds64(B + 8u * ((8 * J + g) * S + l0 + t));  // B(l0+t, 8J+g)
+      for (int J = 0; J < TJ; ++J)
+        fb[J] = J < nj ? lds64(B + 8u * ((8 * (J0 + J) + g) * S + l0 + t)) : 0.0;  // B(l0+t, 8J+g)
 #pragma unroll
-      for (int J = 0; J < T; ++J) dmma(acc[J][0], acc[J][1], fa, fb[J]);
+      for (int J = 0; J < TJ; ++J)
+        if (J < nj) dmma(acc[J][0], acc[J][1], fa, fb[J]);
     }
     __syncwarp();
 #pragma unroll
-    for (int J = 0; J < T; ++J)
+    for (int J = 0; J < TJ; ++J)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
-        if (r < s && c < s) {
+        const int r = 8 * I + g, c = 8 * (J0 + J) + 2 * t + e;
+        if (J < nj && r < s && c < s) {
           const uint32_t off = C + 8u * (c * S + r);
           sts64(off, use_c ? fma(P.alpha, acc[J][e], P.beta * lds64(off)) : P.alpha * acc[J][e]);
         }
@@ -486,7 +494,7 @@ cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b
       if (e != cudaSuccess) return e;                                                                    \
       attr = true;                                                                                       \
     }                                                                                                    \
-    gemm_cm_kernel<TV><<<grid, 32 * TV, smem, st>>>(P);                                                  \
+    gemm_cm_kernel<TV><<<grid, 32 * TV * CM_SPLIT, smem, st>>>(P);                                                  \
     return cudaGetLastError();                                                                           \
   }
   switch (s / 8) {
