@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(256) gemm_tiny4_kernel(const __grid_constant__
 // and the stage count follows shared memory (2 stages up to s = 80, then 1).
 // The engine's 64-wide tiles would waste up to 44 % (s = 48) and 64 % (s = 68)
 // of every tile at these orders.
-template <int T, bool SC, int NST>
-__global__ void __launch_bounds__(32 * T) gemm_mid_kernel(const __grid_constant__ SmallArgs P) {
+template <int T, bool SC, int NST, int SPL>
+__global__ void __launch_bounds__(32 * T * SPL) gemm_mid_kernel(const __grid_constant__ SmallArgs P) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[2];
   constexpr int NOP = SC ? 3 : 2;
@@ -214,35 +214,38 @@ __global__ void __launch_bounds__(32 * T) gemm_mid_kernel(const __grid_constant_
     const double* A = bufp(slot);
     const double* B = A + ss;
     double* Cq = bufp(slot) + 2 * ss;
-    const int I = warp;
+    // SPL warps per row tile, each owning TJ column tiles starting at J0
+    constexpr int TJ = (T + SPL - 1) / SPL;
+    const int I = warp % T, J0 = (warp / T) * TJ, nj = min(TJ, T - J0);
     const double* Cg = P.c + prob * ss;
     double* Dg = P.d + prob * ss;
-    double cpre[SC ? 1 : T][2];  // unstaged C: loaded before the k loop so its latency hides under it
+    double cpre[SC ? 1 : TJ][2];  // unstaged C: loaded before the k loop so its latency hides under it
     if constexpr (!SC) {
 #pragma unroll
-      for (int J = 0; J < T; ++J)
+      for (int J = 0; J < TJ; ++J)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+          const int r = 8 * I + g, c = 8 * (J0 + J) + 2 * t + e;
           const long long off = (long long)(r >> 2) * 4 * s + c * 4 + (r & 3);
-          cpre[J][e] = ldg_if(Cg + off, use_c && r < s && c < s, 0.0);
+          cpre[J][e] = ldg_if(Cg + off, J < nj && use_c && r < s && c < s, 0.0);
         }
     }
-    double acc[T][2];
+    double acc[TJ][2];
 #pragma unroll
-    for (int J = 0; J < T; ++J) acc[J][0] = acc[J][1] = 0.0;
+    for (int J = 0; J < TJ; ++J) acc[J][0] = acc[J][1] = 0.0;
     const int ra = 8 * I + g;
     for (int l0 = 0; l0 < s; l0 += 4) {
       // rows past s read neighbouring data and only feed discarded outputs
       const double fa = A[(long long)(ra >> 2) * 4 * s + (l0 + t) * 4 + (ra & 3)];
-      double fb[T];
+      double fb[TJ];
 #pragma unroll
-      for (int J = 0; J < T; ++J) {
-        const int rb = 8 * J + g;
-        fb[J] = B[(long long)(rb >> 2) * 4 * s + (l0 + t) * 4 + (rb & 3)];
+      for (int J = 0; J < TJ; ++J) {
+        const int rb = 8 * (J0 + J) + g;
+        fb[J] = J < nj ? B[(long long)(rb >> 2) * 4 * s + (l0 + t) * 4 + (rb & 3)] : 0.0;
       }
 #pragma unroll
-      for (int J = 0; J < T; ++J) dmma(acc[J][0], acc[J][1], fa, fb[J]);
+      for (int J = 0; J < TJ; ++J)
+        if (J < nj) dmma(acc[J][0], acc[J][1], fa, fb[J]);
     }
     if (NST == 1) {
       __syncthreads();  // every warp is done with the operands: load the next problem under the epilogue
@@ -251,11 +254,11 @@ __global__ void __launch_bounds__(32 * T) gemm_mid_kernel(const __grid_constant_
       __syncwarp();
     }
 #pragma unroll
-    for (int J = 0; J < T; ++J)
+    for (int J = 0; J < TJ; ++J)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
-        if (r < s && c < s) {
+        const int r = 8 * I + g, c = 8 * (J0 + J) + 2 * t + e;
+        if (J < nj && r < s && c < s) {
           const long long off = (long long)(r >> 2) * 4 * s + c * 4 + (r & 3);
           if constexpr (SC) Cq[off] = use_c ? fma(P.alpha, acc[J][e], P.beta * Cq[off]) : P.alpha * acc[J][e];
           else Dg[off] = use_c ? fma(P.alpha, acc[J][e], P.beta * cpre[J][e]) : P.alpha * acc[J][e];
@@ -275,20 +278,20 @@ __global__ void __launch_bounds__(32 * T) gemm_mid_kernel(const __grid_constant_
   if (SC && tid == 0) bulk_wait_read0();
 }
 
-template <int T, bool SC, int NST>
+template <int T, bool SC, int NST, int SPL = (T <= 8 ? 2 : 1)>
 static cudaError_t mid_t(SmallArgs& P, cudaStream_t st) {
   // + one 4-row panel of slack: the last tile's rows past s read (and discard) past the last operand
   const size_t smem = ((size_t)NST * (SC ? 3 : 2) * P.s * P.s + 4 * (size_t)P.s) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_mid_kernel<T, SC, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_mid_kernel<T, SC, NST, SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int per_sm = std::max(1, (int)((225 * 1024) / (smem + 1024)));
   const int grid = (int)std::min<long long>(P.batch, (long long)per_sm * num_sms());
-  gemm_mid_kernel<T, SC, NST><<<grid, 32 * T, smem, st>>>(P);
+  gemm_mid_kernel<T, SC, NST, SPL><<<grid, 32 * T * SPL, smem, st>>>(P);
   return cudaGetLastError();
 }
 
