@@ -363,16 +363,6 @@ __global__ void scale_kernel(OutDesc o, int m, int n, double beta, int uplo, lon
   }
 }
 
-static int g_sms = 0;
-int num_sms() {
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
-  }
-  return g_sms;
-}
 
 // ------------------------------------------------------------------ tensor maps
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -450,11 +440,9 @@ static cudaError_t launch_t(KParams& P, cudaStream_t s) {
   P.nstages = nst;
   size_t smem = (size_t)nst * stage_bytes + (size_t)nst * 16;
   auto kern = gemm_tiles_kernel<LA, LB, OUT_PM>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = smem_attr((const void*)kern, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   long long grid = std::min<long long>(P.items, (long long)num_sms());
   kern<<<(int)grid, NTHREADS, smem, s>>>(P);

@@ -265,9 +265,9 @@ __global__ void __launch_bounds__(32 * T * SPL) gemm_mid_kernel(const __grid_con
         }
       }
     if (SC) {
+      fence_proxy_async();  // every writer orders its generic-proxy stores before the async-proxy store
       __syncthreads();
       if (tid == 0) {
-        fence_proxy_async();
         bulk_s2g(P.d + prob * ss, smem_u32(Cq), 8u * (uint32_t)ss);
         bulk_commit();
       }
@@ -282,12 +282,9 @@ template <int T, bool SC, int NST, int SPL = (T <= 8 ? 2 : 1)>
 static cudaError_t mid_t(SmallArgs& P, cudaStream_t st) {
   // + one 4-row panel of slack: the last tile's rows past s read (and discard) past the last operand
   const size_t smem = ((size_t)NST * (SC ? 3 : 2) * P.s * P.s + 4 * (size_t)P.s) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_mid_kernel<T, SC, NST, SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         220 * 1024);
+  {
+    cudaError_t e = smem_attr((const void*)gemm_mid_kernel<T, SC, NST, SPL>, 220 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int per_sm = std::max(1, (int)((225 * 1024) / (smem + 1024)));
   const int grid = (int)std::min<long long>(P.batch, (long long)per_sm * num_sms());
@@ -324,12 +321,9 @@ static cudaError_t mid_launch(SmallArgs& P, cudaStream_t st) {
 template <int T>
 static cudaError_t small_t(SmallArgs& P, cudaStream_t st) {
   const size_t smem = 2 * 3 * (size_t)P.G * P.s * P.s * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_small_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         110 * 1024);
+  {
+    cudaError_t e = smem_attr((const void*)gemm_small_kernel<T>, 110 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int grid = (int)std::min<long long>(P.nchunks, 2LL * num_sms());
   gemm_small_kernel<T><<<grid, 32 * SM_WARPS, smem, st>>>(P);
@@ -490,12 +484,9 @@ cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b
   const int grid = (int)std::min<long long>(batch, (long long)per_sm * num_sms());
 #define PB_CM(TV)                                                                                        \
   case TV: {                                                                                             \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      cudaError_t e = cudaFuncSetAttribute(gemm_cm_kernel<TV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                           220 * 1024);                                                  \
+    {                                                                                                    \
+      cudaError_t e = smem_attr((const void*)gemm_cm_kernel<TV>, 220 * 1024);                            \
       if (e != cudaSuccess) return e;                                                                    \
-      attr = true;                                                                                       \
     }                                                                                                    \
     gemm_cm_kernel<TV><<<grid, 32 * TV * CM_SPLIT, smem, st>>>(P);                                                  \
     return cudaGetLastError();                                                                           \

@@ -194,12 +194,9 @@ static cudaError_t getrf_smem(double* a, long long stride, int lda, int m, int n
   P.S = lu_stride((m + 7) & ~7);
   size_t smem = (size_t)P.S * ((n + 7) & ~7) * sizeof(double);
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(getrf_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         220 * 1024);
+  {
+    cudaError_t e = smem_attr((const void*)getrf_smem_kernel, 220 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int mx = std::max(m, n);
   int threads = mx <= 32 ? 64 : (mx <= 64 ? 128 : 256);

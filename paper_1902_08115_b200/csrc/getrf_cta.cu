@@ -294,12 +294,9 @@ __global__ void __launch_bounds__(32 * (NU + 1)) getrf_cta_kernel(const __grid_c
 template <int R, int NU>
 static cudaError_t getrf_cta_t(const GetrfCtaArgs& P, int batch, cudaStream_t s) {
   const size_t smem = (size_t)P.S * ((P.n + 7) & ~7) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(getrf_cta_kernel<R, NU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         220 * 1024);
+  {
+    cudaError_t e = smem_attr((const void*)getrf_cta_kernel<R, NU>, 220 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   getrf_cta_kernel<R, NU><<<(unsigned)batch, 32 * (NU + 1), smem, s>>>(P);
   return cudaGetLastError();

@@ -48,7 +48,10 @@ cudaError_t gemm_launch(const GemmLaunch& g, cudaStream_t s);
 cudaError_t scale_launch(int out_pm, const OutDesc& o, int m, int n, double beta, int uplo,
                          int batch, cudaStream_t s);
 
+// Per-device runtime state (runtime.cpp, thread-safe): SM count, and the
+// >48 KB dynamic shared-memory opt-in of a kernel on the current device.
 int num_sms();
+cudaError_t smem_attr(const void* fn, int bytes, bool max_carveout = false);
 
 // small-size panel-major NT gemm (s <= 32, packed problems): gemm_small.cu
 bool gemm_small_ok(int s, const double* a, const double* b, const double* c, const double* d, long long sa,
@@ -77,9 +80,6 @@ struct PotrfLaunch {
   int batch = 0;
 };
 cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s);
-// register-resident warp-per-problem Cholesky, n <= 64 (potrf_warp.cu)
-cudaError_t potrf_warp_launch(double* a, long long stride, int lda, int n, int upper, int* info,
-                              int info_offset, int skip_nonzero, int batch, cudaStream_t s);
 // pipelined left-looking CTA-per-problem Cholesky, n <= 160 (potrf_cta.cu)
 cudaError_t potrf_cta_launch(double* a, long long stride, const long long* offs, const int* nvec, int lda,
                              int n, int upper, int pm, int zero_fill, int* info, int info_offset,
@@ -99,10 +99,6 @@ cudaError_t syrk_potrf_cta_launch(double* d, long long stride_d, const long long
 // step), A n x n in the same storage kind, n <= 160
 cudaError_t syrk_lower_cta_launch(double* c, const long long* offs, const int* nvec, const double* A, int nmax,
                                   int pm, int* info, int batch, cudaStream_t s);
-// panel-major (ps = 4) variant; offs/nvec optional (variable batches, ld = round_up(n, 4));
-// zero_fill writes the LowerZero band zeros of syrk_potrf_nd
-cudaError_t potrf_warp_pm_launch(double* a, long long stride, const long long* offs, const int* nvec,
-                                 int cn, int n, int zero_fill, int* info, int batch, cudaStream_t s);
 
 // LU with partial pivoting (dgetrf, in place).
 struct GetrfLaunch {
@@ -164,10 +160,13 @@ struct TrsmLaunch {
   const long long* offs_b = nullptr;
 };
 cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s);
+// panel-major trsm_rltn_nd with alpha == 0: zero-diagonal report, then D = +0 (trsm.cu)
+cudaError_t trsm_nd_zero_launch(const TrsmLaunch& L, cudaStream_t s);
 // warp-per-8-rows left-looking DMMA solve for X * A^T = alpha B, A lower (trsm_rlt.cu);
 // trsm_launch forwards these flag sets
 bool trsm_rlt_ok(const TrsmLaunch& L);
-// keep the default stream-ordered memory pool's memory between calls (scratch reuse)
+// keep the default stream-ordered memory pool's memory between calls (scratch reuse;
+// once per device, runtime.cpp)
 void mempool_keep();
 cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s);
 

@@ -56,6 +56,13 @@ int status(pb_result* res, int info, const char* msg) {
   }
   return info;
 }
+// Numerical failure of a factorization: the reference still reports the
+// flop count (factor.hpp:93, 222-223 set flops after the failure status).
+int numerical(pb_result* res, int info, const char* msg, long long flops) {
+  status(res, info, msg);
+  if (res) res->flops = flops;
+  return info;
+}
 int cuda_fail(pb_result* res, const char* routine, cudaError_t e) {
   cudaGetLastError();
   if (res) {
@@ -221,11 +228,11 @@ int run_batched(const char* routine, std::vector<Operand> ops, int batch, pb_str
   const size_t target = (size_t)48 << 20;
   long long chunk = std::max<long long>(1, std::min<long long>(batch, (long long)(target / std::max<size_t>(per, 1))));
   int nchunks = (int)((batch + chunk - 1) / chunk);
-  // Do not start before earlier work on the caller's stream has finished.
-  if (stream) {
-    e = cudaStreamSynchronize((cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_fail(res, routine, e);
-  }
+  // Do not start before earlier work on the caller's stream (NULL: the legacy
+  // default stream, which the non-blocking staging streams do not wait for)
+  // has finished: it may still be writing the host buffers.
+  e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(res, routine, e);
   for (int c = 0; c < nchunks; ++c) {
     int s = c & 1;
     long long p0 = (long long)c * chunk, nb = std::min<long long>(chunk, batch - p0);
@@ -554,6 +561,7 @@ static int dpotrf_impl(bool batched, char uplo, int n, double* a, int lda, long 
   if (batched) {
     if (batch < 0) return fail(res, routine, 5, -5, "batch is negative");
     if (sa < 0) return fail(res, routine, 6, -6, "a stride is negative");
+    if (!info && n > 0 && batch > 0) return fail(res, routine, 7, -7, "info is null");
   }
   long long flops = (long long)n * n * n / 3 * batch;  // factor.hpp:93
   if (n == 0 || batch == 0) {
@@ -589,7 +597,7 @@ static int dpotrf_impl(bool batched, char uplo, int n, double* a, int lda, long 
     single_info = cell.host;
   }
   if (rc) return rc;
-  if (!batched && single_info) return status(res, single_info, "matrix is not positive definite");
+  if (!batched && single_info) return numerical(res, single_info, "matrix is not positive definite", flops);
   return finish(res, 0, flops);
 }
 
@@ -613,9 +621,11 @@ static int dgetrf_impl(bool batched, int m, int n, double* a, int lda, long long
   if (batched) {
     if (batch < 0) return fail(res, routine, 7, -7, "batch is negative");
     if (sa < 0 || sp < minmn) return fail(res, routine, 8, -8, "a stride is negative or ipiv stride below min(m, n)");
+    if (!ipiv && minmn > 0 && batch > 0) return fail(res, routine, 9, -9, "ipiv is null");
+    if (!info && minmn > 0 && batch > 0) return fail(res, routine, 10, -10, "info is null");
   }
-  long long p = minmn, q = std::max(m, n);
-  long long flops = (p * p * q - p * p * p / 3) * batch;  // bench.hpp:132-136 / factor.hpp:222
+  // BlasResult.flops of the reference (factor.hpp:222-223): n^2 m - n^3/3
+  long long flops = ((long long)n * n * m - (long long)n * n * n / 3) * batch;
   if (minmn == 0 || batch == 0) {
     if (batched && info && batch > 0) {
       if (kind_of(info) == K_DEVICE) cudaMemsetAsync(info, 0, sizeof(int) * batch, (cudaStream_t)stream);
@@ -627,7 +637,9 @@ static int dgetrf_impl(bool batched, int m, int n, double* a, int lda, long long
   int* infop = batched ? info : &cell.host;
   std::vector<Operand> ops(3);
   ops[0] = {(void*)a, 8, sa, cm_extent(m, n, lda), true, true};
-  ops[1] = {(void*)ipiv, 4, batched ? sp : minmn, minmn, false, true};
+  // ipiv rows with gaps (stride > min(m, n)) are staged in too, so the
+  // entries between problems survive the host round trip
+  ops[1] = {(void*)ipiv, 4, batched ? sp : minmn, minmn, batched && sp != minmn, true};
   ops[2] = {(void*)infop, 4, 1, 1, false, true};
   if (!batched && kind_of(a) == K_DEVICE) {
     if (cudaMalloc(&cell.dev, sizeof(int)) != cudaSuccess) return cuda_fail(res, routine, cudaGetLastError());
@@ -651,10 +663,7 @@ static int dgetrf_impl(bool batched, int m, int n, double* a, int lda, long long
     single_info = cell.host;
   }
   if (rc) return rc;
-  if (!batched && single_info) {
-    if (res) { finish(res, single_info, 0); res->message = "factor has an exactly zero pivot"; }
-    return single_info;
-  }
+  if (!batched && single_info) return numerical(res, single_info, "factor has an exactly zero pivot", flops);
   return finish(res, 0, flops);
 }
 
@@ -846,6 +855,7 @@ static int trsm_rltn_nd_impl(bool batched, int m, int n, double alpha, pb_dmat a
                          L.b = alias ? L.d : (const double*)p[1]; L.sb = sb; L.ldb = b.cn;
                          L.info = (int*)p[3];
                          L.batch = nb;
+                         if (alpha == 0.0) return trsm_nd_zero_launch(L, s);  // level3.hpp:493-504
                          return trsm_launch(L, s);
                        });
   int single_info = 0;
@@ -880,6 +890,7 @@ static int syrk_potrf_nd_impl(bool batched, int n, int k, pb_dmat a, long long s
   if (!panel_ok(c, n, n)) return status(res, -6, "c panel mismatch");
   if (!panel_ok(d, n, n)) return status(res, -7, "d panel mismatch");
   if (batched && batch < 0) return status(res, -13, "batch is negative");
+  if (batched && !info && n > 0 && batch > 0) return status(res, -14, "info is null");
   if (n == 0 || batch == 0) {
     if (batched && info && batch > 0) {
       if (kind_of(info) == K_DEVICE) cudaMemsetAsync(info, 0, sizeof(int) * batch, (cudaStream_t)stream);

@@ -563,9 +563,8 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
   } else if (!PM && !P.upper && !zf && (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0) && (n % 2 == 0)) {
     // one TMA bulk store per column for the 16-byte aligned part of rows [col, rlim);
     // an odd first row goes alone (its pair partner is in the opposite triangle)
-    // one TMA bulk store per column for the 16-byte aligned part of rows [col, rlim);
-    // an odd first row goes alone (its pair partner is in the opposite triangle)
-    fence_proxy_async();
+    fence_proxy_async();  // writers fence, then the barrier, then the async-proxy stores
+    __syncthreads();
     for (int col = tid; col < ncols; col += NTH) {
       const int kb = col >> 3, c = col & 7, r0 = 8 * kb;
       const int rlim = fail ? (col >= band_cols ? band_lo : band_lo + 8) : n;
@@ -602,15 +601,10 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
 template <int T, int NU, int PM>
 static cudaError_t cta_launch_t(const PotrfCtaArgs& P, cudaStream_t s) {
   const size_t smem = (size_t)(cta_pbase(T, T) + 8 * T + 32) * sizeof(double);  // + panel-warp read slack
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(potrf_cta_kernel<T, NU, PM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+  {
     // residency is bounded by shared memory: ask for the largest carveout
-    e = cudaFuncSetAttribute(potrf_cta_kernel<T, NU, PM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaError_t e = smem_attr((const void*)potrf_cta_kernel<T, NU, PM>, (int)smem, true);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   potrf_cta_kernel<T, NU, PM><<<(unsigned)P.batch, 32 * (NU + 1), smem, s>>>(P);
   return cudaGetLastError();

@@ -179,6 +179,35 @@ __global__ void __launch_bounds__(256) trsm_kernel(const __grid_constant__ TrsmA
   if (rb == 0 && tid == 0 && !L.skip_nonzero && L.info) L.info[p] = 0;
 }
 
+// trsm_rltn_nd with alpha == 0 (level3.hpp:493-504): the exact-zero diagonal
+// test still runs first and reports before any store; otherwise D's m x n
+// entries become +0 (scale_tiles_nd with beta 0: B is never read, pad lanes
+// untouched).  One CTA per problem, panel-major operands.
+__global__ void __launch_bounds__(256) trsm_nd_zero_kernel(const __grid_constant__ TrsmLaunch L) {
+  __shared__ int sh_zero;
+  const int p = blockIdx.x, tid = threadIdx.x;
+  const double* A = L.a + (long long)p * L.sa;
+  double* D = L.d + (long long)p * L.sd;
+  if (tid == 0) sh_zero = 0x7fffffff;
+  __syncthreads();
+  for (int i = tid; i < L.nn; i += blockDim.x)
+    if (A[aoff<1>(L.lda, i, i)] == 0.0) atomicMin(&sh_zero, i + 1);
+  __syncthreads();
+  const int z = sh_zero == 0x7fffffff ? 0 : sh_zero;
+  if (tid == 0 && L.info) L.info[p] = z;
+  if (z) return;
+  for (int e = tid; e < L.mm * L.nn; e += blockDim.x) {
+    const int c = e / L.mm, r = e - c * L.mm;
+    D[aoff<1>(L.ldd, r, c)] = 0.0;
+  }
+}
+
+cudaError_t trsm_nd_zero_launch(const TrsmLaunch& L, cudaStream_t s) {
+  if (L.batch <= 0 || L.mm <= 0 || L.nn <= 0) return cudaSuccess;
+  trsm_nd_zero_kernel<<<(unsigned)L.batch, 256, 0, s>>>(L);
+  return cudaGetLastError();
+}
+
 cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.mm <= 0 || L.nn <= 0) return cudaSuccess;
   static const bool rlt = [] {  // PBGPU_TRSM_RLT=0 keeps this kernel for every flag set (A/B)
@@ -192,13 +221,9 @@ cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s) {
   T.nn8 = (L.nn + 7) & ~7;
   size_t smem = (size_t)(TR_SX + TR_SP) * T.nn8 * sizeof(double);
   if (smem > 220 * 1024) return cudaErrorInvalidValue;  // nn <= 340
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(trsm_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  {
+    cudaError_t e = smem_attr((const void*)(L.pm ? trsm_kernel<1> : trsm_kernel<0>), 220 * 1024);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(trsm_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
   }
   long long grid = (long long)L.batch * T.rowblocks;
   if (L.pm)

@@ -241,21 +241,6 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
   if (rb == 0 && lane == 0 && L.info && !L.skip_nonzero) L.info[p] = 0;
 }
 
-// Stream-ordered scratch (cudaMallocAsync) stays cheap only if the default
-// pool keeps its memory between calls instead of releasing it at every
-// synchronization: raise the release threshold once per device.
-void mempool_keep() {
-  static int done_dev = -1;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  cudaGetLastError();
-  done_dev = dev;
-}
 
 bool trsm_rlt_ok(const TrsmLaunch& L) { return !(L.twin && L.pm) && L.lower && L.trans && L.nn <= 512; }
 // (offs_b is honoured only here: trsm_launch forwards every such launch to this kernel)
@@ -274,13 +259,9 @@ cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
   // (measured: no gain up to 8 tiles, 1.2x at 16, 1.6x at 32)
   const int ntr = !reg_ok || R.ntmax <= 8 || R.ntmax > 32 ? 0 : ((R.ntmax + 3) & ~3);  // a multiple of 4 tiles
   const size_t smem = (size_t)((ntr ? 0 : kRltWarps) + 2) * R.ntmax * 64 * sizeof(double);  // [X slices +] 2 staged A rows
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(trsm_rlt_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(trsm_rlt_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaError_t e = cudaGetLastError();
+  {
+    cudaError_t e = smem_attr((const void*)(L.pm ? trsm_rlt_kernel<1, 0> : trsm_rlt_kernel<0, 0>), 200 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const unsigned grid = (unsigned)((long long)L.batch * ((R.rbmax + kRltWarps - 1) / kRltWarps));
   mempool_keep();

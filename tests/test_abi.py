@@ -121,3 +121,19 @@ def test_no_cpu_fallback_without_device(pb):
     a = np.asfortranarray(np.eye(4))
     with pytest.raises(RuntimeError, match="no CUDA device"):
         pb.dgemm("n", "n", 4, 4, 4, 1.0, a, 4, a, 4, 0.0, a.copy(order="F"), 4)
+
+
+def test_batched_null_info_rejected(pb):
+    """Batched factorizations write info[p] per problem: a null info (or ipiv) is an
+    argument error reported before anything is launched (extension argument positions)."""
+    buf = np.zeros(64)
+    r = pb.dpotrf_batched("l", 4, buf, 4, 16, None, 2)
+    assert r.info == -7 and r.error.index == 7
+    ip = np.zeros(8, np.int32); info = np.zeros(2, np.int32)
+    r = pb.dgetrf_batched(4, 4, buf, 4, 16, None, 4, info, 2)
+    assert r.info == -9 and r.error.index == 9
+    r = pb.dgetrf_batched(4, 4, buf, 4, 16, ip, 4, None, 2)
+    assert r.info == -10 and r.error.index == 10
+    P = pb.PanelRef
+    r = pb.syrk_potrf_nd_batched(4, 0, P(buf, 4, 0), 0, P(buf, 4, 0), 0, P(buf, 4, 4), 16, P(buf, 4, 4), 16, None, 2)
+    assert r.info == -14

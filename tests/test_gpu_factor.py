@@ -213,3 +213,54 @@ def test_trsm_rltn_nd(pb, orc):
         io = bp.copy()
         assert pb.trsm_rltn_nd(m, n, 1.5, pb.PanelRef(ap, n, n), pb.PanelRef(io, m, n), pb.PanelRef(io, m, n)).ok()
         assert rel_frob(unpack(io, m, n), unpack(want, m, n)) <= tol(n)
+
+
+def test_trsm_rltn_nd_alpha_zero(pb, orc):
+    """level3.hpp:493-504: alpha == 0 -> zero-diagonal check first, then +0 without reading B."""
+    rng = np.random.default_rng(5)
+    m, n = 9, 12
+    A = make_tri(rng, "l", "n", n)
+    ap = pack(A, fill=np.nan)
+    bp = pack(np.full((m, n), np.inf), fill=np.nan)
+    bp[::3] = np.nan
+    d = np.full(panel_len(m, n), 4.25)
+    want = d.copy()
+    assert pb.trsm_rltn_nd(m, n, 0.0, pb.PanelRef(ap, n, n), pb.PanelRef(bp, m, n), pb.PanelRef(d, m, n)).ok()
+    assert orc.trsm_rltn_nd(m, n, 0.0, dmat(ap, n, n), dmat(bp, m, n), dmat(want, m, n)) == 0
+    assert same_bits(d, want)                       # +0 in the m x n entries, pad lanes untouched
+    # a zero diagonal is still reported before any write
+    A2 = A.copy(order="F"); A2[4, 4] = 0.0
+    ap2 = pack(A2, fill=np.nan)
+    d2 = np.full(panel_len(m, n), -3.5)
+    r = pb.trsm_rltn_nd(m, n, 0.0, pb.PanelRef(ap2, n, n), pb.PanelRef(bp, m, n), pb.PanelRef(d2, m, n))
+    assert r.info == 5 and (d2 == -3.5).all()
+    # batched on the device, per-problem info
+    import torch
+    batch = 3
+    L = panel_len(m, n)
+    As = torch.from_numpy(np.stack([ap, ap2, ap])).cuda()
+    Bs = torch.from_numpy(np.stack([bp] * batch)).cuda()
+    Ds = torch.full((batch, L), 7.0, dtype=torch.float64, device="cuda")
+    info = torch.full((batch,), -9, dtype=torch.int32, device="cuda")
+    P = pb.PanelRef
+    assert pb.trsm_rltn_nd_batched(m, n, 0.0, P(As, n, n), n * n, P(Bs, m, n), L, P(Ds, m, n), L, info, batch).ok()
+    assert info.cpu().tolist() == [0, 5, 0]
+    out = Ds.cpu().numpy()
+    assert same_bits(out[0], want) and same_bits(out[2], want) and (out[1] == 7.0).all()
+
+
+def test_dgetrf_host_ipiv_stride_gaps(pb, orc):
+    """Strided host ipiv (stride > min(m, n)): the entries between problems survive."""
+    rng = np.random.default_rng(17)
+    n, batch, sp = 12, 5, 20
+    A = rng.uniform(-1, 1, (batch, n, n))
+    a = np.ascontiguousarray(A).reshape(-1).copy()
+    ipiv = np.full(batch * sp, -77, np.int32)
+    info = np.full(batch, 9, np.int32)
+    assert pb.dgetrf_batched(n, n, a, n, n * n, ipiv, sp, info, batch).ok()
+    assert (info == 0).all()
+    for p in range(batch):
+        w = F(A[p].T); wp = np.zeros(n, np.int32)
+        orc.dgetrf(n, n, ptr(w), n, ptr(wp))
+        assert np.array_equal(ipiv[p * sp:p * sp + n], wp)
+        assert (ipiv[p * sp + n:(p + 1) * sp] == -77).all()
