@@ -20,7 +20,10 @@
  *     PB_INFO_UNSUPPORTED = kInfoUnsupported (gemm.hpp:183).
  * Batched factorizations/solves report per-problem numerical failures in the
  * caller's info[batch] array (same memory kind as the matrices) and return 0
- * from the call itself unless an argument is invalid.
+ * from the call itself unless an argument is invalid.  Arguments the
+ * reference signature has keep the reference's position in error reports;
+ * the batched extensions (strides, batch, info, ipiv) report positions
+ * after them.  info (and ipiv) of the batched factorizations must not be NULL.
  */
 #ifndef PBGPU_H
 #define PBGPU_H
@@ -132,6 +135,56 @@ int pb_syrk_potrf_nd_batched(int n, int k, pb_dmat a, long long stride_a, pb_dma
 int pb_chain_vbatched(char layout, const int* n, const long long* offset, double* A, double* C,
                       double* B, int* info, int batch, int max_n, pb_stream stream,
                       pb_result* res);
+
+/* ---------------- triangular multiply (completes the six-routine surface) ---------------- */
+/* replaces panelblas::dtrmm (blas.hpp:166-176 -> level3.hpp:250-275): B <- alpha op(A) B
+ * (side 'l') or alpha B op(A) (side 'r'); validation shared with dtrsm (blas.hpp:132-162) */
+int pb_dtrmm(char side, char uplo, char transa, char diag, int m, int n, double alpha,
+             const double* a, int lda, double* b, int ldb, pb_result* res);
+int pb_dtrmm_batched(char side, char uplo, char transa, char diag, int m, int n, double alpha,
+                     const double* a, int lda, long long stride_a, double* b, int ldb,
+                     long long stride_b, int batch, pb_stream stream, pb_result* res);
+/* replaces panelblas::trmm_rlnn_nd (level3.hpp:446-479): d <- alpha b a, a lower non-unit;
+ * b may alias d exactly */
+int pb_trmm_rlnn_nd(int m, int n, double alpha, pb_dmat a, pb_dmat b, pb_dmat d, pb_result* res);
+int pb_trmm_rlnn_nd_batched(int m, int n, double alpha, pb_dmat a, long long stride_a, pb_dmat b,
+                            long long stride_b, pb_dmat d, long long stride_d, int batch,
+                            pb_stream stream, pb_result* res);
+
+/* ---------------- layout conversion on the device (panel_mat.hpp:45-48, 141-171) ---------------- */
+/* replaces panelblas::memsize (panel_mat.hpp:45-48): bytes of an m x n matrix packed with height ps */
+long long pb_memsize(int m, int n, int ps);
+/* replaces pack_from_colmajor (panel_mat.hpp:141-160): d <- packed op(a), op(a) is d.m x d.n,
+ * any panel height d.ps; pad lanes of d are never written */
+int pb_pack(char trans, const double* a, int lda, pb_dmat d, pb_result* res);
+int pb_pack_batched(char trans, const double* a, int lda, long long stride_a, pb_dmat d,
+                    long long stride_d, int batch, pb_stream stream, pb_result* res);
+/* replaces unpack_to_colmajor (panel_mat.hpp:164-171): a (s.m x s.n, ld lda) <- s */
+int pb_unpack(pb_dmat s, double* a, int lda, pb_result* res);
+int pb_unpack_batched(pb_dmat s, long long stride_s, double* a, int lda, long long stride_a,
+                      int batch, pb_stream stream, pb_result* res);
+
+/* ---------------- batched factorized Riccati recursion (the paper's application) ----------------
+ * replaces, for a batch of independent OCPs with equal (nx, nu, N), RiccatiFusedWork's stage loop
+ * as riccati_run's FusedNative path drives it (riccati.hpp:257-373, 402-512).  Panel-major, ps = 4:
+ *   m0 (nt x nt, nt = nx + nu): bordered stage matrix [[R, S], [S^T, Q]], packed fully symmetric;
+ *   q (nx x nx): Q;  g (nt x nx): G = [B^T; A^T].
+ * calL_N = chol(Q); for s = N-1 .. 0: C = G calL_{s+1} (trmm_rlnn_nd),
+ * F_s = chol(m0 + C C^T) (syrk_potrf_nd), calL_s = trailing nx x nx block of F_s.
+ * f receives the N stage factors F_s of problem p at f.data + p*stride_f + s*f.pm*f.cn (lower,
+ * crossing tiles zero-filled, strictly-upper tiles zero: [[Lambda, 0], [L, calL]]);
+ * lterm (optional, data may be NULL) receives calL_N.  info[p] = 0 or the failing pivot's
+ * 1-based bordered index (riccati.hpp:234-278); stage[p] (optional) = the failing stage, N for
+ * the terminal factor, -1 when none failed.  Stages below a failed one are unspecified. */
+int pb_riccati_nd_batched(int nx, int nu, int N, pb_dmat m0, long long stride_m0, pb_dmat q,
+                          long long stride_q, pb_dmat g, long long stride_g, pb_dmat f,
+                          long long stride_f, pb_dmat lterm, long long stride_lterm, int* info,
+                          int* stage, int batch, pb_stream stream, pb_result* res);
+
+/* Fault injection: with the environment variable PBGPU_MUTATE=eps set when the library is
+ * loaded, every routine adds eps to element (0, 0) of each problem's result (the analogue of
+ * PANELBLAS_MUTATE, gemm.hpp:126-127, micro_kernel.hpp:424-426) — a negative control that
+ * must turn the parity harness red. */
 
 #ifdef __cplusplus
 }

@@ -82,9 +82,13 @@ _SIGS = {
                            _LL, _I]),
     "dpotrf_batch": (None, [_CH, _I, _P, _I, _LL, _P, _LL, _I]),
     "dgetrf_batch": (None, [_I, _I, _P, _I, _LL, _P, _LL, _P, _LL, _I]),
+    "dtrmm": (_I, [_CH, _CH, _CH, _CH, _I, _I, _D, _P, _I, _P, _I]),
+    "trmm_rlnn_nd": (_I, [_I, _I, _D, Dmat, Dmat, Dmat]),
+    "gemm_nd_batch": (None, [_CH, _CH, _I, _I, _I, _D, Dmat, _LL, Dmat, _LL, _D, Dmat, _LL, Dmat,
+                             _LL, _LL, _I]),
+    "chain_batch": (None, [_I, _P, _P, _P, _P, _P, _P, _LL, _I]),
 }
 _REF_ONLY = {
-    "dtrmm": (_I, [_CH, _CH, _CH, _CH, _I, _I, _D, _P, _I, _P, _I]),
     "naive_gemm": (None, [_CH, _CH, _I, _I, _I, _D, _P, _I, _P, _I, _D, _P, _I]),
     "naive_potrf": (_I, [_CH, _I, _P, _I]),
     "naive_getrf": (_I, [_I, _I, _P, _I, _P]),
@@ -94,10 +98,17 @@ _REF_ONLY = {
     "make_spd": (None, [_I, C.c_uint64, _P]),
     "hw_threads": (_I, []),
     "last_error_index": (_I, []),
-    "gemm_nd_batch": (None, [_CH, _CH, _I, _I, _I, _D, Dmat, _LL, Dmat, _LL, _D, Dmat, _LL, Dmat,
-                             _LL, _LL, _I]),
     "chain_cm_batch": (None, [_P, _P, _P, _P, _P, _P, _LL, _I]),
     "chain_pm_batch": (None, [_P, _P, _P, _P, _P, _P, _LL, _I]),
+    "pack_from_colmajor": (None, [_CH, _P, _I, _I, _I, Dmat]),
+    "unpack_to_colmajor": (None, [Dmat, _P, _I]),
+    "memsize": (_LL, [_I, _I, _I]),
+    "make_ocp_data": (None, [_I, _I, C.c_uint64, _P, _P, _P, _P, _P]),
+    "riccati_fused": (_I, [_I, _I, _I, C.c_uint64, _P, _P, C.POINTER(_I)]),
+    "riccati_run": (_D, [_I, _I, _I, _I, C.c_uint64, C.POINTER(_I)]),
+    "chol_residual": (_D, [_I, _P, _I, _P, _I]),
+    "riccati_oracle_step": (_I, [_I, _I, C.c_uint64, _P, _P]),
+    "riccati_seed": (C.c_uint64, []),
 }
 
 

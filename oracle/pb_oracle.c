@@ -184,6 +184,67 @@ int orc_dtrsm(char side, char uplo, char transa, char diag, int m, int n, double
   return 0;
 }
 
+/* ------------------------------------------------------------------ dtrmm */
+/* Right-side multiply core, level3.hpp:132-170 (trmm_right_core) +
+ * kernel_trmm_right micro_kernel.hpp:566-586 + edge_trmm_right 357-378.
+ * For each NR-column tile of the effective problem: t = 0; t += X(r,l) *
+ * opA(l, j0+c) over the rectangular range (l ascending: [j0+na, nn) when
+ * op(A) is effectively lower, [0, j0) when upper); then the triangular edge
+ * l in [j0+c, j0+na) (eff. lower) or [j0, j0+c] (eff. upper), unit diagonals
+ * counted as 1 and never read; then scale_ab(alpha, 0) = t * alpha.  The
+ * row band of X is packed before any tile of that band is stored, so b may
+ * be the destination. */
+static void trmm_right_rows(const trsm_ctx* s, int lower, int unit, int mm, int nn, double alpha,
+                            double* xrow) {
+  int eff_lower = lower == !s->trans;
+  double t[NR];
+  for (int r = 0; r < mm; ++r) {
+    for (int l = 0; l < nn; ++l) xrow[l] = *tx(s, r, l); /* pack_row_block */
+    for (int j0 = 0; j0 < nn; j0 += NR) {
+      int na = imin(NR, nn - j0);
+      int l0 = eff_lower ? j0 + na : 0, l1 = eff_lower ? nn : j0;
+      for (int c = 0; c < na; ++c) {
+        double acc = 0.0;
+        for (int l = l0; l < l1; ++l) acc += xrow[l] * topa(s, l, j0 + c);
+        int lo = eff_lower ? c : 0, hi = eff_lower ? na : c + 1;
+        for (int l = lo; l < hi; ++l) {
+          double f = (l == c && unit) ? 1.0 : topa(s, j0 + l, j0 + c);
+          acc += xrow[j0 + l] * f;
+        }
+        t[c] = acc * alpha;
+      }
+      for (int c = 0; c < na; ++c) *tx(s, r, j0 + c) = t[c];
+    }
+  }
+}
+
+/* blas.hpp:166-176 (trimul_adapter 133-162, same validation as dtrsm) ->
+ * level3.hpp:250-275. */
+int orc_dtrmm(char side, char uplo, char transa, char diag, int m, int n, double alpha,
+              const double* a, int lda, double* b, int ldb) {
+  int sd = p_side(side), lo = p_uplo(uplo), tr = p_trans(transa), un = p_diag(diag);
+  if (sd < 0) return 1;
+  if (lo < 0) return 2;
+  if (tr < 0) return 3;
+  if (un < 0) return 4;
+  if (m < 0) return 5;
+  if (n < 0) return 6;
+  int t = sd ? m : n;
+  if (lda < imax(1, t)) return 9;
+  if (ldb < imax(1, m)) return 11;
+  if (m == 0 || n == 0) return 0;
+  if (alpha == 0.0) { /* scale_only(beta = 0): zeros, a never read */
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < m; ++i) CM(b, ldb, i, j) = 0.0 * 0.0;
+    return 0;
+  }
+  trsm_ctx s = {b, ldb, sd, a, lda, sd ? !tr : tr};
+  double* xrow = (double*)malloc(sizeof(double) * (size_t)imax(1, t));
+  trmm_right_rows(&s, lo, un, sd ? n : m, sd ? m : n, alpha, xrow);
+  free(xrow);
+  return 0;
+}
+
 /* ----------------------------------------------------------------- dpotrf */
 /* blas.hpp:190-202 -> factor.hpp:45-99 (potrf_core) with
  * kernel_potrf_sub/_diag (micro_kernel.hpp:607-636), edge_potrf 309-325 and
@@ -424,6 +485,43 @@ int orc_trsm_rltn_nd(int m, int n, double alpha, orc_dmat a, orc_dmat b, orc_dma
   return 0;
 }
 
+/* level3.hpp:446-479 + kernel_trmm_right_p micro_kernel.hpp:588-601:
+ * d <- alpha * b * a, a lower non-unit, untransposed (effectively lower):
+ * per NR-column tile, the rectangular part l in [j0+na, n) (inner_gemm_nn_pp,
+ * l ascending), then the edge l in [j0+c, j0+na), then t * alpha.  b may
+ * alias d: each tile reads columns at or right of its own and the sweep
+ * stores left to right, so rows are staged before they are overwritten. */
+int orc_trmm_rlnn_nd(int m, int n, double alpha, orc_dmat a, orc_dmat b, orc_dmat d) {
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  if (!panel_ok(a, n, n)) return -5;
+  if (!panel_ok(b, m, n)) return -6;
+  if (!panel_ok(d, m, n)) return -7;
+  if (m == 0 || n == 0) return 0;
+  if (alpha == 0.0) {
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < m; ++i) PM(d, i, j) = 0.0 * 0.0;
+    return 0;
+  }
+  double* xrow = (double*)malloc(sizeof(double) * (size_t)n);
+  double t[NR];
+  for (int r = 0; r < m; ++r) {
+    for (int l = 0; l < n; ++l) xrow[l] = PM(b, r, l);
+    for (int j0 = 0; j0 < n; j0 += NR) {
+      int na = imin(NR, n - j0);
+      for (int c = 0; c < na; ++c) {
+        double acc = 0.0;
+        for (int l = j0 + na; l < n; ++l) acc += xrow[l] * PM(a, l, j0 + c);
+        for (int l = c; l < na; ++l) acc += xrow[j0 + l] * PM(a, j0 + l, j0 + c);
+        t[c] = acc * alpha;
+      }
+      for (int c = 0; c < na; ++c) PM(d, r, j0 + c) = t[c];
+    }
+  }
+  free(xrow);
+  return 0;
+}
+
 /* level3.hpp:533-575 + kernel_syrk_potrf_sub/_diag micro_kernel.hpp:640-673:
  * lower d <- chol(c + a b^T), left-looking; tile value before the edge is
  * (c(i,j) - sum_{l<j0} D(i,l) D(j,l)) + a(i,0) b(j,0) + ... (l ascending);
@@ -542,4 +640,49 @@ void orc_dgetrf_batch(int m, int n, double* a, int lda, long long sa, int* ipiv,
                       int* info, long long batch, int threads) {
   fac_args f = {'l', m, n, lda, a, sa, ipiv, sipiv, info};
   par_for(batch, threads, getrf_one, &f);
+}
+
+typedef struct {
+  char ta, tb; int m, n, k; double alpha, beta;
+  orc_dmat a, b, c, d; long long sa, sb, sc, sd;
+} gemm_nd_args;
+static void gemm_nd_one(long long p, void* v) {
+  gemm_nd_args* g = (gemm_nd_args*)v;
+  orc_dmat a = g->a, b = g->b, c = g->c, d = g->d;
+  a.data += p * g->sa; b.data += p * g->sb; c.data += p * g->sc; d.data += p * g->sd;
+  orc_gemm_nd(g->ta, g->tb, g->m, g->n, g->k, g->alpha, a, b, g->beta, c, d);
+}
+void orc_gemm_nd_batch(char ta, char tb, int m, int n, int k, double alpha, orc_dmat a, long long sa,
+                       orc_dmat b, long long sb, double beta, orc_dmat c, long long sc, orc_dmat d,
+                       long long sd, long long batch, int threads) {
+  gemm_nd_args g = {ta, tb, m, n, k, alpha, beta, a, b, c, d, sa, sb, sc, sd};
+  par_for(batch, threads, gemm_nd_one, &g);
+}
+
+/* Config-5 chain per problem (the reference's own
+ * calls, as ref_shim.cpp's ref_chain_*_batch):
+ *   cm: dsyrk('l','n') C += A A^T; dpotrf('l') C; dtrsm('r','l','t','n') X L^T = B
+ *   pm: syrk_potrf_nd(n, n, A, A, C, C); trsm_rltn_nd(n, n, 1, C, B, B) */
+typedef struct { const int* nv; const long long* off; double *A, *C, *B; int* info; int pm; } chain_args;
+static orc_dmat pmat(double* p, int n) { orc_dmat d = {p, PS, n, n, (n + PS - 1) / PS * PS, (n + PS - 1) / PS * PS}; return d; }
+static void chain_one(long long p, void* v) {
+  chain_args* c = (chain_args*)v;
+  int n = c->nv[p];
+  double *a = c->A + c->off[p], *cc = c->C + c->off[p], *b = c->B + c->off[p];
+  int inf;
+  if (!c->pm) {
+    orc_dsyrk('l', 'n', n, n, 1.0, a, n, 1.0, cc, n);
+    inf = orc_dpotrf('l', n, cc, n);
+    if (inf == 0) inf = orc_dtrsm('r', 'l', 't', 'n', n, n, 1.0, cc, n, b, n);
+  } else {
+    orc_dmat A = pmat(a, n), C = pmat(cc, n), B = pmat(b, n);
+    inf = orc_syrk_potrf_nd(n, n, A, A, C, C);
+    if (inf == 0) inf = orc_trsm_rltn_nd(n, n, 1.0, C, B, B);
+  }
+  c->info[p] = inf;
+}
+void orc_chain_batch(int pm, const int* nvec, const long long* off, double* A, double* C, double* B,
+                     int* info, long long batch, int threads) {
+  chain_args c = {nvec, off, A, C, B, info, pm};
+  par_for(batch, threads, chain_one, &c);
 }

@@ -30,6 +30,8 @@ int orc_dsyrk(char uplo, char trans, int n, int k, double alpha, const double* a
               double beta, double* c, int ldc);
 int orc_dtrsm(char side, char uplo, char transa, char diag, int m, int n, double alpha,
               const double* a, int lda, double* b, int ldb);
+int orc_dtrmm(char side, char uplo, char transa, char diag, int m, int n, double alpha,
+              const double* a, int lda, double* b, int ldb);
 int orc_dpotrf(char uplo, int n, double* a, int lda);
 int orc_dgetrf(int m, int n, double* a, int lda, int* ipiv);
 
@@ -38,6 +40,7 @@ int orc_gemm_nd(char transa, char transb, int m, int n, int k, double alpha, orc
 int orc_syrk_nd(int n, int k, double alpha, orc_dmat a, double beta, orc_dmat c, orc_dmat d);
 int orc_trsm_rltn_nd(int m, int n, double alpha, orc_dmat a, orc_dmat b, orc_dmat d);
 int orc_syrk_potrf_nd(int n, int k, orc_dmat a, orc_dmat b, orc_dmat c, orc_dmat d);
+int orc_trmm_rlnn_nd(int m, int n, double alpha, orc_dmat a, orc_dmat b, orc_dmat d);
 
 /* Threaded batch loops (contiguous split) — the "port" CPU baseline. */
 void orc_dgemm_batch(char ta, char tb, int m, int n, int k, double alpha, const double* a, int lda,
@@ -47,6 +50,12 @@ void orc_dpotrf_batch(char uplo, int n, double* a, int lda, long long sa, int* i
                       long long batch, int threads);
 void orc_dgetrf_batch(int m, int n, double* a, int lda, long long sa, int* ipiv, long long sipiv,
                       int* info, long long batch, int threads);
+void orc_gemm_nd_batch(char ta, char tb, int m, int n, int k, double alpha, orc_dmat a, long long sa,
+                       orc_dmat b, long long sb, double beta, orc_dmat c, long long sc, orc_dmat d,
+                       long long sd, long long batch, int threads);
+/* config-5 chain, pm = 0 column-major / 1 panel-major, offsets in doubles */
+void orc_chain_batch(int pm, const int* nvec, const long long* off, double* A, double* C, double* B,
+                     int* info, long long batch, int threads);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@
 #include "panelblas/blas.hpp"
 #include "panelblas/matgen.hpp"
 #include "panelblas/reference.hpp"
+#include "panelblas/riccati.hpp"
 
 using namespace panelblas;
 
@@ -216,5 +217,74 @@ void ref_chain_pm_batch(const int* nvec, const long long* off_nn, double* A, dou
     info[p] = inf;
   });
 }
+
+
+// ---- (e) trmm_rlnn_nd, pack, and the Riccati application (riccati.hpp) ----
+int ref_trmm_rlnn_nd(int m, int n, double alpha, ref_dmat a, ref_dmat b, ref_dmat d) {
+  EngineConfig cfg;
+  g_err_index = 0;
+  return trmm_rlnn_nd(cfg, m, n, alpha, cpr(a), cpr(b), pr(d)).status.info;
+}
+void ref_pack_from_colmajor(char trans, const double* a, int lda, int am, int an, ref_dmat d) {
+  pack_from_colmajor(ConstMatView{a, am, an, lda}, pr(d), tr(trans));
+}
+void ref_unpack_to_colmajor(ref_dmat s, double* a, int lda) {
+  unpack_to_colmajor(cpr(s), MatView{a, s.m, s.n, lda});
+}
+long long ref_memsize(int m, int n, int ps) { return (long long)memsize(m, n, ps); }
+// make_ocp_data (riccati.hpp:65-103): column-major a (nx x nx), b (nx x nu), q, r, s (nu x nx)
+void ref_make_ocp_data(int nx, int nu, uint64_t seed, double* a, double* b, double* q, double* r, double* s) {
+  OcpData d = make_ocp_data(nx, nu, seed);
+  std::memcpy(a, d.a.data(), sizeof(double) * nx * nx);
+  if (nu) std::memcpy(b, d.b.data(), sizeof(double) * nx * nu);
+  std::memcpy(q, d.q.data(), sizeof(double) * nx * nx);
+  if (nu) std::memcpy(r, d.r.data(), sizeof(double) * nu * nu);
+  if (nu) std::memcpy(s, d.s.data(), sizeof(double) * nu * nx);
+}
+// RiccatiFusedWork on make_ocp_data(seed): init_terminal, then N steps.  Stage s's bordered
+// factor [[Lambda, 0], [L, calL]] lands column-major (nt x nt, zeros above) at fst + s*nt*nt,
+// the terminal factor calL_N at lterm (nx x nx).  Returns status.info; *fail_stage = the
+// failing stage (N for the terminal factor) or -1.
+int ref_riccati_fused(int nx, int nu, int N, uint64_t seed, double* fst, double* lterm, int* fail_stage) {
+  OcpData d = make_ocp_data(nx, nu, seed);
+  EngineConfig cfg;
+  RiccatiFusedWork w(d, cfg);
+  const int nt = nx + nu;
+  *fail_stage = -1;
+  Status st = w.init_terminal();
+  if (!st.ok()) { *fail_stage = N; return st.info; }
+  Matrix c0 = w.call_cm();
+  std::memcpy(lterm, c0.data(), sizeof(double) * nx * nx);
+  for (int n = N - 1; n >= 0; --n) {
+    RiccatiStepResult r = w.step();
+    if (!r.ok()) { *fail_stage = n; return r.status.info; }
+    double* out = fst + (long long)n * nt * nt;
+    std::memset(out, 0, sizeof(double) * nt * nt);
+    Matrix lam = w.lambda_cm(), l = w.l_cm(), cl = w.call_cm();
+    for (int j = 0; j < nu; ++j)
+      for (int i = j; i < nu; ++i) out[i + j * nt] = lam(i, j);
+    for (int j = 0; j < nu; ++j)
+      for (int i = 0; i < nx; ++i) out[nu + i + j * nt] = l(i, j);
+    for (int j = 0; j < nx; ++j)
+      for (int i = j; i < nx; ++i) out[nu + i + (nu + j) * nt] = cl(i, j);
+  }
+  return 0;
+}
+// riccati_run (riccati.hpp:402-512): impl 0 blas, 1 fused, 2 oracle; returns the residual.
+double ref_riccati_run(int nx, int nu, int N, int impl, uint64_t seed, int* info) {
+  RiccatiRunResult r = riccati_run(OcpDims{nx, nu, N}, static_cast<RiccatiImpl>(impl), seed);
+  *info = r.status.info;
+  return r.residual;
+}
+// chol_residual (riccati.hpp:124-140), column-major
+double ref_chol_residual(int n, const double* l, int ldl, const double* p, int ldp) {
+  return chol_residual(ConstMatView{l, n, n, ldl}, ConstMatView{p, n, n, ldp});
+}
+// riccati_oracle_step (riccati.hpp:145-180) on make_ocp_data(seed): p <- step(pnext), cm nx x nx
+int ref_riccati_oracle_step(int nx, int nu, uint64_t seed, const double* pnext, double* p) {
+  OcpData d = make_ocp_data(nx, nu, seed);
+  return riccati_oracle_step(d, ConstMatView{pnext, nx, nx, nx}, MatView{p, nx, nx, nx}).info;
+}
+uint64_t ref_riccati_seed() { return kRiccatiSeed; }
 
 }  // extern "C"

@@ -26,7 +26,9 @@ __all__ = [
     "gemm_nd", "syrk_nd", "trsm_rltn_nd", "syrk_potrf_nd",
     "dgemm_batched", "dsyrk_batched", "dtrsm_batched", "dpotrf_batched", "dgetrf_batched",
     "gemm_nd_batched", "syrk_nd_batched", "trsm_rltn_nd_batched", "syrk_potrf_nd_batched",
-    "chain_vbatched", "INFO_UNSUPPORTED", "INFO_CUDA_ERROR", "INFO_NO_DEVICE",
+    "chain_vbatched", "dtrmm", "dtrmm_batched", "trmm_rlnn_nd", "trmm_rlnn_nd_batched",
+    "memsize", "pack", "pack_batched", "unpack", "unpack_batched", "riccati_nd_batched",
+    "INFO_UNSUPPORTED", "INFO_CUDA_ERROR", "INFO_NO_DEVICE",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -77,6 +79,17 @@ _SIGS = {
     "pb_syrk_potrf_nd_batched": (_I, [_I, _I, _Dmat, _LL, _Dmat, _LL, _Dmat, _LL, _Dmat, _LL, _P,
                                       _I, _P, _R]),
     "pb_chain_vbatched": (_I, [_CH, _P, _P, _P, _P, _P, _P, _I, _I, _P, _R]),
+    "pb_dtrmm": (_I, [_CH, _CH, _CH, _CH, _I, _I, _D, _P, _I, _P, _I, _R]),
+    "pb_dtrmm_batched": (_I, [_CH, _CH, _CH, _CH, _I, _I, _D, _P, _I, _LL, _P, _I, _LL, _I, _P, _R]),
+    "pb_trmm_rlnn_nd": (_I, [_I, _I, _D, _Dmat, _Dmat, _Dmat, _R]),
+    "pb_trmm_rlnn_nd_batched": (_I, [_I, _I, _D, _Dmat, _LL, _Dmat, _LL, _Dmat, _LL, _I, _P, _R]),
+    "pb_memsize": (_LL, [_I, _I, _I]),
+    "pb_pack": (_I, [_CH, _P, _I, _Dmat, _R]),
+    "pb_pack_batched": (_I, [_CH, _P, _I, _LL, _Dmat, _LL, _I, _P, _R]),
+    "pb_unpack": (_I, [_Dmat, _P, _I, _R]),
+    "pb_unpack_batched": (_I, [_Dmat, _LL, _P, _I, _LL, _I, _P, _R]),
+    "pb_riccati_nd_batched": (_I, [_I, _I, _I, _Dmat, _LL, _Dmat, _LL, _Dmat, _LL, _Dmat, _LL, _Dmat,
+                                   _LL, _P, _P, _I, _P, _R]),
 }
 
 #: every symbol include/pbgpu.h declares (checked by tests/test_abi.py)
@@ -339,4 +352,84 @@ def chain_vbatched(layout, n, offset, A, C_, B, info, batch, max_n, stream=None)
     r = _Result()
     lib().pb_chain_vbatched(_ch(layout), _ptr(n), _ptr(offset), _ptr(A), _ptr(C_), _ptr(B), _ptr(info),
                             batch, max_n, _stream(stream), C.byref(r))
+    return _result(_DEFAULT, r)
+
+
+# ------------------------------------------------------- dtrmm / trmm_rlnn_nd
+def dtrmm(side, uplo, transa, diag, m, n, alpha, a, lda, b, ldb, cfg: BlasConfig = _DEFAULT):
+    """blas.hpp:166-176: B <- alpha op(A) B (side 'l') or alpha B op(A) (side 'r')."""
+    r = _Result()
+    lib().pb_dtrmm(_ch(side), _ch(uplo), _ch(transa), _ch(diag), m, n, alpha, _ptr(a), lda, _ptr(b),
+                   ldb, C.byref(r))
+    return _result(cfg, r)
+
+
+def dtrmm_batched(side, uplo, transa, diag, m, n, alpha, a, lda, stride_a, b, ldb, stride_b, batch,
+                  stream=None, cfg: BlasConfig = _DEFAULT):
+    r = _Result()
+    lib().pb_dtrmm_batched(_ch(side), _ch(uplo), _ch(transa), _ch(diag), m, n, alpha, _ptr(a), lda,
+                           stride_a, _ptr(b), ldb, stride_b, batch, _stream(stream), C.byref(r))
+    return _result(cfg, r)
+
+
+def trmm_rlnn_nd(m, n, alpha, a: PanelRef, b: PanelRef, d: PanelRef):
+    """level3.hpp:446-479: d <- alpha b a, a lower non-unit."""
+    r = _Result()
+    lib().pb_trmm_rlnn_nd(m, n, alpha, a.c(), b.c(), d.c(), C.byref(r))
+    return _result(_DEFAULT, r)
+
+
+def trmm_rlnn_nd_batched(m, n, alpha, a: PanelRef, stride_a, b: PanelRef, stride_b, d: PanelRef,
+                         stride_d, batch, stream=None):
+    r = _Result()
+    lib().pb_trmm_rlnn_nd_batched(m, n, alpha, a.c(), stride_a, b.c(), stride_b, d.c(), stride_d,
+                                  batch, _stream(stream), C.byref(r))
+    return _result(_DEFAULT, r)
+
+
+# ------------------------------------------------------------- pack / unpack
+def memsize(m, n, ps=4) -> int:
+    """panel_mat.hpp:45-48."""
+    return int(lib().pb_memsize(m, n, ps))
+
+
+def pack(trans, a, lda, d: PanelRef, cfg: BlasConfig = _DEFAULT):
+    """panel_mat.hpp:141-160: d <- packed op(a); pad lanes untouched."""
+    r = _Result()
+    lib().pb_pack(_ch(trans), _ptr(a), lda, d.c(), C.byref(r))
+    return _result(cfg, r)
+
+
+def pack_batched(trans, a, lda, stride_a, d: PanelRef, stride_d, batch, stream=None,
+                 cfg: BlasConfig = _DEFAULT):
+    r = _Result()
+    lib().pb_pack_batched(_ch(trans), _ptr(a), lda, stride_a, d.c(), stride_d, batch, _stream(stream),
+                          C.byref(r))
+    return _result(cfg, r)
+
+
+def unpack(s: PanelRef, a, lda, cfg: BlasConfig = _DEFAULT):
+    """panel_mat.hpp:164-171: a <- unpacked s."""
+    r = _Result()
+    lib().pb_unpack(s.c(), _ptr(a), lda, C.byref(r))
+    return _result(cfg, r)
+
+
+def unpack_batched(s: PanelRef, stride_s, a, lda, stride_a, batch, stream=None,
+                   cfg: BlasConfig = _DEFAULT):
+    r = _Result()
+    lib().pb_unpack_batched(s.c(), stride_s, _ptr(a), lda, stride_a, batch, _stream(stream), C.byref(r))
+    return _result(cfg, r)
+
+
+# ------------------------------------------------------------------ Riccati
+def riccati_nd_batched(nx, nu, N, m0: PanelRef, stride_m0, q: PanelRef, stride_q, g: PanelRef,
+                       stride_g, f: PanelRef, stride_f, lterm: Optional[PanelRef], stride_lterm,
+                       info, stage, batch, stream=None):
+    """Batched RiccatiFusedWork stage loop (riccati.hpp:257-373, 402-512); see include/pbgpu.h."""
+    r = _Result()
+    lt = lterm.c() if lterm is not None else _Dmat(None, 4, nx, nx, _round_up(nx, 4), _round_up(nx, 4))
+    lib().pb_riccati_nd_batched(nx, nu, N, m0.c(), stride_m0, q.c(), stride_q, g.c(), stride_g, f.c(),
+                                stride_f, lt, stride_lterm, _ptr(info), _ptr(stage), batch,
+                                _stream(stream), C.byref(r))
     return _result(_DEFAULT, r)

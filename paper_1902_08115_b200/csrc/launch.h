@@ -160,6 +160,10 @@ struct TrsmLaunch {
   const long long* offs_b = nullptr;
 };
 cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s);
+// Triangular multiply D = alpha * X * op(A) over the same effective right-side
+// problem as TrsmLaunch (info / skip / nvec / offs ignored): dtrmm (all flag
+// sets, Left as twin) and the panel-major trmm_rlnn_nd; D may alias B (trmm.cu)
+cudaError_t trmm_launch(const TrsmLaunch& L, cudaStream_t s);
 // panel-major trsm_rltn_nd with alpha == 0: zero-diagonal report, then D = +0 (trsm.cu)
 cudaError_t trsm_nd_zero_launch(const TrsmLaunch& L, cudaStream_t s);
 // warp-per-8-rows left-looking DMMA solve for X * A^T = alpha B, A lower (trsm_rlt.cu);
@@ -192,6 +196,33 @@ struct ChainLaunch {
   int batch = 0, max_n = 0;
 };
 cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s);
+
+// Batched factorized Riccati recursion (riccati.cu): panel-major (ps = 4)
+// operands, uniform dims; f holds N stage factors per OCP (stage s at
+// f + p*sf + s*cnf*cnf), lterm (optional) the terminal factor chol(Q).
+struct RiccatiLaunch {
+  int nx = 0, nu = 0, N = 0;
+  const double* m0 = nullptr; long long sm0 = 0; int cnm0 = 0;  // nt x nt bordered matrix
+  const double* q = nullptr; long long sq = 0; int cnq = 0;     // nx x nx
+  const double* g = nullptr; long long sg = 0; int cng = 0;     // nt x nx, [B^T; A^T]
+  double* f = nullptr; long long sf = 0; int cnf = 0;           // N x (nt x nt)
+  double* lterm = nullptr; long long sl = 0; int cnl = 0;       // nx x nx
+  int* info = nullptr;
+  int* stage = nullptr;
+  int batch = 0;
+};
+cudaError_t riccati_launch(const RiccatiLaunch& R, cudaStream_t s);
+
+// Layout kernels (layout.cu): batched pack (column-major op(A) -> panel-major,
+// any ps, pad lanes untouched) and unpack (panel-major -> column-major).
+cudaError_t pack_launch(int trans, int m, int n, const double* a, int lda, long long sa, double* d, int ps,
+                        int cn, long long sd, int batch, cudaStream_t s);
+cudaError_t unpack_launch(int m, int n, const double* src, int ps, int cn, long long ss, double* a, int lda,
+                          long long sa, int batch, cudaStream_t s);
+// Fault injection (PBGPU_MUTATE, the analogue of PANELBLAS_MUTATE, gemm.hpp:126-127 /
+// micro_kernel.hpp:424-426): adds eps to element (0, 0) of each problem's result.
+double mutation_epsilon();
+cudaError_t mutate_launch(double* d, long long sd, const long long* offs, int batch, double eps, cudaStream_t s);
 
 double probe_dmma_tflops();
 

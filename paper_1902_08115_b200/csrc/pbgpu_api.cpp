@@ -200,9 +200,21 @@ size_t region_bytes(const Operand& o, long long nb) {
 
 // Runs launch(ptrs, nb, stream) over the batch.  Device operands run in one
 // launch on the caller's stream; host operands are staged in chunks.
+//
+// `result` names the operand holding the routine's result: under
+// PBGPU_MUTATE=eps (fault injection, the analogue of PANELBLAS_MUTATE,
+// gemm.hpp:126-127) element (0, 0) of every problem's result is perturbed
+// by eps after the launch, so the parity harness can be shown to go red.
 template <class F>
 int run_batched(const char* routine, std::vector<Operand> ops, int batch, pb_stream stream,
-                pb_result* res, F&& launch) {
+                pb_result* res, int result, F&& launch) {
+  const double eps = mutation_epsilon();
+  auto run = [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
+    cudaError_t e = launch(p, nb, s);
+    if (e == cudaSuccess && eps != 0.0 && result >= 0 && p[result])
+      e = mutate_launch((double*)p[result], ops[result].stride, nullptr, nb, eps, s);
+    return e;
+  };
   if (!device_ok()) return status(res, PB_INFO_NO_DEVICE, "no CUDA device: pbgpu has no CPU path");
   int ndev = 0, nhost = 0;
   for (auto& o : ops) {
@@ -214,7 +226,7 @@ int run_batched(const char* routine, std::vector<Operand> ops, int batch, pb_str
   std::vector<void*> ptrs(ops.size());
   if (!nhost) {
     for (size_t i = 0; i < ops.size(); ++i) ptrs[i] = ops[i].ptr;
-    cudaError_t e = launch(ptrs, batch, (cudaStream_t)stream);
+    cudaError_t e = run(ptrs, batch, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(res, routine, e);
     return 0;
   }
@@ -250,7 +262,7 @@ int run_batched(const char* routine, std::vector<Operand> ops, int batch, pb_str
         if (e != cudaSuccess) return cuda_fail(res, routine, e);
       }
     }
-    e = launch(ptrs, (int)nb, S.st[s]);
+    e = run(ptrs, (int)nb, S.st[s]);
     if (e != cudaSuccess) return cuda_fail(res, routine, e);
     for (size_t i = 0; i < ops.size(); ++i) {
       const Operand& o = ops[i];
@@ -348,7 +360,7 @@ static int dgemm_impl(const char* routine, bool batched, char transa, char trans
   ops[1] = {(void*)b, 8, sb, scale_only ? 0 : cm_extent(nrowb, tb == 0 ? n : k, ldb), true, false};
   ops[2] = {(void*)c, 8, sc, cm_extent(m, n, ldc), beta != 0.0 || !dense(m, ldc, sc, n, batch), true};
   if (scale_only) ops[0].ptr = ops[1].ptr = nullptr;
-  int rc = run_batched(routine, ops, batch, stream, res,
+  int rc = run_batched(routine, ops, batch, stream, res, 2,
                        [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
                          OutDesc o;
                          o.c = (const double*)p[2];
@@ -418,7 +430,7 @@ static int dsyrk_impl(bool batched, char uplo, char trans, int n, int k, double 
   ops[0] = {(void*)a, 8, sa, scale_only ? 0 : cm_extent(nrowa, tr == 0 ? k : n, lda), true, false};
   ops[1] = {(void*)c, 8, sc, cm_extent(n, n, ldc), true, true};
   if (scale_only) ops[0].ptr = nullptr;
-  int rc = run_batched(routine, ops, batch, stream, res,
+  int rc = run_batched(routine, ops, batch, stream, res, 1,
                        [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
                          OutDesc o;
                          o.c = (const double*)p[1];
@@ -498,7 +510,7 @@ static int dtrsm_impl(bool batched, char side, char uplo, char transa, char diag
     if (cudaMalloc(&cell.dev, sizeof(int)) != cudaSuccess) return cuda_fail(res, routine, cudaGetLastError());
     ops[2].ptr = cell.dev;
   }
-  int rc = run_batched(routine, ops, batch, stream, res,
+  int rc = run_batched(routine, ops, batch, stream, res, 1,
                        [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
                          if (alpha == 0.0) {  // level3.hpp:291: zeros, a never read
                            OutDesc o;
@@ -580,7 +592,7 @@ static int dpotrf_impl(bool batched, char uplo, int n, double* a, int lda, long 
     if (cudaMalloc(&cell.dev, sizeof(int)) != cudaSuccess) return cuda_fail(res, routine, cudaGetLastError());
     ops[1].ptr = cell.dev;
   }
-  int rc = run_batched(routine, ops, batch, stream, res,
+  int rc = run_batched(routine, ops, batch, stream, res, 0,
                        [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
                          PotrfLaunch L;
                          L.a = (double*)p[0]; L.stride = sa; L.lda = lda; L.n = n;
@@ -646,7 +658,7 @@ static int dgetrf_impl(bool batched, int m, int n, double* a, int lda, long long
     ops[2].ptr = cell.dev;
   }
   long long spv = batched ? sp : minmn;
-  int rc = run_batched(routine, ops, batch, stream, res,
+  int rc = run_batched(routine, ops, batch, stream, res, 0,
                        [&](const std::vector<void*>& pt, int nb, cudaStream_t s) -> cudaError_t {
                          GetrfLaunch L;
                          L.a = (double*)pt[0]; L.stride = sa; L.lda = lda; L.m = m; L.n = n;
@@ -716,7 +728,7 @@ static int gemm_nd_impl(bool batched, char transa, char transb, int m, int n, in
   ops[3] = {(void*)d.data, 8, sd, pm_extent(d), true, true};  // pad lanes must survive the round trip
   if (scale_only) ops[0].ptr = ops[1].ptr = nullptr;
   if (alias || beta == 0.0) ops[2].ptr = nullptr;
-  int rc = run_batched("gemm_nd", ops, batch, stream, res,
+  int rc = run_batched("gemm_nd", ops, batch, stream, res, 3,
                        [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
                          OutDesc o;
                          o.d = (double*)p[3];
@@ -779,7 +791,7 @@ static int syrk_nd_impl(bool batched, int n, int k, double alpha, pb_dmat a, lon
   ops[2] = {(void*)d.data, 8, sd, pm_extent(d), true, true};
   if (scale_only) ops[0].ptr = nullptr;
   if (alias || beta == 0.0) ops[1].ptr = nullptr;
-  int rc = run_batched("syrk_nd", ops, batch, stream, res,
+  int rc = run_batched("syrk_nd", ops, batch, stream, res, 2,
                        [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
                          OutDesc o;
                          o.d = (double*)p[2];
@@ -843,7 +855,7 @@ static int trsm_rltn_nd_impl(bool batched, int m, int n, double alpha, pb_dmat a
     if (cudaMalloc(&cell.dev, sizeof(int)) != cudaSuccess) return cuda_fail(res, "trsm_rltn_nd", cudaGetLastError());
     ops[3].ptr = cell.dev;
   }
-  int rc = run_batched("trsm_rltn_nd", ops, batch, stream, res,
+  int rc = run_batched("trsm_rltn_nd", ops, batch, stream, res, 2,
                        [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
                          TrsmLaunch L;
                          L.pm = 1;
@@ -913,7 +925,7 @@ static int syrk_potrf_nd_impl(bool batched, int n, int k, pb_dmat a, long long s
     if (cudaMalloc(&cell.dev, sizeof(int)) != cudaSuccess) return cuda_fail(res, "syrk_potrf_nd", cudaGetLastError());
     ops[4].ptr = cell.dev;
   }
-  int rc = run_batched("syrk_potrf_nd", ops, batch, stream, res,
+  int rc = run_batched("syrk_potrf_nd", ops, batch, stream, res, 3,
                        [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
                          SyrkPotrfLaunch L;
                          L.a = (const double*)p[0]; L.sa = sa; L.cna = a.cn;
@@ -972,8 +984,257 @@ int pb_chain_vbatched(char layout, const int* n, const long long* offset, double
   L.info = info;
   L.batch = batch; L.max_n = max_n;
   cudaError_t e = chain_launch(L, (cudaStream_t)stream);
+  if (e == cudaSuccess && mutation_epsilon() != 0.0)
+    e = mutate_launch(B, 0, offset, batch, mutation_epsilon(), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(res, routine, e);
   return finish(res, 0, 0);
+}
+
+
+// ============================================================== dtrmm
+// blas.hpp:166-176: the trimul adapter shared with dtrsm (blas.hpp:132-162),
+// same validation order and positions; level3.hpp:250-275 underneath.
+static int dtrmm_impl(bool batched, char side, char uplo, char transa, char diag, int m, int n,
+                      double alpha, const double* a, int lda, long long sa, double* b, int ldb,
+                      long long sb, int batch, pb_stream stream, pb_result* res) {
+  const char* routine = "dtrmm";
+  int sd = parse_side(side);
+  if (sd < 0) return fail(res, routine, 1, 1, "side is not one of l, r");
+  int lo = parse_uplo(uplo);
+  if (lo < 0) return fail(res, routine, 2, 2, "uplo is not one of u, l");
+  int tr = parse_trans(transa);
+  if (tr < 0) return fail(res, routine, 3, 3, "transa is not one of n, t, c");
+  int un = parse_diag(diag);
+  if (un < 0) return fail(res, routine, 4, 4, "diag is not one of u, n");
+  if (m < 0) return fail(res, routine, 5, 5, "m is negative");
+  if (n < 0) return fail(res, routine, 6, 6, "n is negative");
+  int nrowa = sd ? m : n;
+  if (lda < std::max(1, nrowa)) return fail(res, routine, 9, 9, "lda is smaller than the triangle order");
+  if (ldb < std::max(1, m)) return fail(res, routine, 11, 11, "ldb is smaller than m");
+  if (batched) {
+    if (batch < 0) return fail(res, routine, 12, 12, "batch is negative");
+    if (sa < 0 || sb < 0) return fail(res, routine, 13, 13, "a stride is negative");
+  }
+  if (m == 0 || n == 0 || batch == 0) return finish(res, 0, 0);
+  const long long flops = alpha == 0.0 ? 0 : (sd ? (long long)n * m * m : (long long)m * n * n) * batch;
+  std::vector<Operand> ops(2);
+  ops[0] = {(void*)a, 8, sa, alpha == 0.0 ? 0 : cm_extent(nrowa, nrowa, lda), true, false};
+  if (alpha == 0.0) ops[0].ptr = nullptr;
+  ops[1] = {(void*)b, 8, sb, cm_extent(m, n, ldb), alpha != 0.0 || !dense(m, ldb, sb, n, batch), true};
+  int rc = run_batched(routine, ops, batch, stream, res, 1,
+                       [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
+                         if (alpha == 0.0) {  // level3.hpp:261: scale_only, zeros, a never read
+                           OutDesc o;
+                           o.c = o.d = (double*)p[1];
+                           o.sc = o.sd = sb;
+                           o.ldc = o.ldd = ldb;
+                           return scale_launch(0, o, m, n, 0.0, 0, nb, s);
+                         }
+                         TrsmLaunch L;
+                         L.pm = 0;
+                         L.twin = sd;
+                         L.lower = lo;
+                         L.trans = sd ? !tr : tr;  // Left = transposed right-side problem (level3.hpp:263-265)
+                         L.unit = un;
+                         L.mm = sd ? n : m;
+                         L.nn = sd ? m : n;
+                         L.alpha = alpha;
+                         L.a = (const double*)p[0]; L.sa = sa; L.lda = lda;
+                         L.b = (const double*)p[1]; L.sb = sb; L.ldb = ldb;
+                         L.d = (double*)p[1]; L.sd = sb; L.ldd = ldb;
+                         L.batch = nb;
+                         return trmm_launch(L, s);
+                       });
+  if (rc) return rc;
+  return finish(res, 0, flops);
+}
+
+int pb_dtrmm(char side, char uplo, char transa, char diag, int m, int n, double alpha,
+             const double* a, int lda, double* b, int ldb, pb_result* res) {
+  return dtrmm_impl(false, side, uplo, transa, diag, m, n, alpha, a, lda, 0, b, ldb, 0, 1, nullptr, res);
+}
+int pb_dtrmm_batched(char side, char uplo, char transa, char diag, int m, int n, double alpha,
+                     const double* a, int lda, long long stride_a, double* b, int ldb,
+                     long long stride_b, int batch, pb_stream stream, pb_result* res) {
+  return dtrmm_impl(true, side, uplo, transa, diag, m, n, alpha, a, lda, stride_a, b, ldb, stride_b,
+                    batch, stream, res);
+}
+
+// ============================================================== trmm_rlnn_nd
+// level3.hpp:446-479: d <- alpha * b * a, a lower non-unit untransposed; b may alias d.
+static int trmm_rlnn_nd_impl(bool batched, int m, int n, double alpha, pb_dmat a, long long sa,
+                             pb_dmat b, long long sb, pb_dmat d, long long sd, int batch,
+                             pb_stream stream, pb_result* res) {
+  if (m < 0) return status(res, -2, "m < 0");
+  if (n < 0) return status(res, -3, "n < 0");
+  if (!panel_ok(a, n, n)) return status(res, -5, "a panel mismatch");
+  if (!panel_ok(b, m, n)) return status(res, -6, "b panel mismatch");
+  if (!panel_ok(d, m, n)) return status(res, -7, "d panel mismatch");
+  if (batched && batch < 0) return status(res, -11, "batch is negative");
+  if (m == 0 || n == 0 || batch == 0) return finish(res, 0, 0);
+  const bool alias = b.data == d.data && sb == sd;
+  std::vector<Operand> ops(3);
+  ops[0] = {(void*)a.data, 8, sa, alpha == 0.0 ? 0 : pm_extent(a), true, false};
+  ops[1] = {(void*)b.data, 8, sb, pm_extent(b), alpha != 0.0, false};
+  ops[2] = {(void*)d.data, 8, sd, pm_extent(d), true, true};  // pad lanes survive the round trip
+  if (alpha == 0.0) ops[0].ptr = ops[1].ptr = nullptr;
+  if (alias) ops[1].ptr = nullptr;
+  int rc = run_batched("trmm_rlnn_nd", ops, batch, stream, res, 2,
+                       [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
+                         if (alpha == 0.0) {  // scale_tiles_nd(beta = 0): +0, b never read
+                           OutDesc o;
+                           o.c = o.d = (double*)p[2];
+                           o.sc = o.sd = sd;
+                           o.ldc = o.ldd = d.cn;
+                           return scale_launch(1, o, m, n, 0.0, 0, nb, s);
+                         }
+                         TrsmLaunch L;
+                         L.pm = 1;
+                         L.lower = 1; L.trans = 0; L.unit = 0;
+                         L.mm = m; L.nn = n;
+                         L.alpha = alpha;
+                         L.a = (const double*)p[0]; L.sa = sa; L.lda = a.cn;
+                         L.d = (double*)p[2]; L.sd = sd; L.ldd = d.cn;
+                         L.b = alias ? L.d : (const double*)p[1]; L.sb = sb; L.ldb = b.cn;
+                         L.batch = nb;
+                         return trmm_launch(L, s);
+                       });
+  if (rc) return rc;
+  return finish(res, 0, alpha == 0.0 ? 0 : (long long)m * n * n * batch);
+}
+
+int pb_trmm_rlnn_nd(int m, int n, double alpha, pb_dmat a, pb_dmat b, pb_dmat d, pb_result* res) {
+  return trmm_rlnn_nd_impl(false, m, n, alpha, a, 0, b, 0, d, 0, 1, nullptr, res);
+}
+int pb_trmm_rlnn_nd_batched(int m, int n, double alpha, pb_dmat a, long long stride_a, pb_dmat b,
+                            long long stride_b, pb_dmat d, long long stride_d, int batch,
+                            pb_stream stream, pb_result* res) {
+  return trmm_rlnn_nd_impl(true, m, n, alpha, a, stride_a, b, stride_b, d, stride_d, batch, stream, res);
+}
+
+// ============================================================== pack / unpack
+// panel_mat.hpp:45-48
+long long pb_memsize(int m, int n, int ps) {
+  if (m <= 0 || n <= 0 || ps <= 0) return 0;
+  return (long long)((m + ps - 1) / ps * ps) * ((n + ps - 1) / ps * ps) * (long long)sizeof(double);
+}
+
+static bool dmat_shape_ok(const pb_dmat& d) {
+  return d.data && d.ps > 0 && d.m >= 0 && d.n >= 0 && d.pm == (d.m + d.ps - 1) / d.ps * d.ps &&
+         d.cn == (d.n + d.ps - 1) / d.ps * d.ps;
+}
+
+// panel_mat.hpp:141-160: d <- packed op(a); op(a) is d.m x d.n; pad lanes untouched.
+static int pack_impl(bool batched, char trans, const double* a, int lda, long long sa, pb_dmat d,
+                     long long sd, int batch, pb_stream stream, pb_result* res) {
+  const char* routine = "pack_from_colmajor";
+  int tr = parse_trans(trans);
+  if (tr < 0) return fail(res, routine, 1, 1, "trans is not one of n, t, c");
+  if (!dmat_shape_ok(d)) return fail(res, routine, 4, 4, "destination is not a consistent panel descriptor");
+  const int rows = tr ? d.n : d.m, cols = tr ? d.m : d.n;
+  if (lda < std::max(1, rows)) return fail(res, routine, 3, 3, "lda is smaller than the rows of a");
+  if (batched) {
+    if (batch < 0) return fail(res, routine, 6, 6, "batch is negative");
+    if (sa < 0 || sd < 0) return fail(res, routine, 7, 7, "a stride is negative");
+  }
+  if (d.m == 0 || d.n == 0 || batch == 0) return finish(res, 0, 0);
+  std::vector<Operand> ops(2);
+  ops[0] = {(void*)a, 8, sa, cm_extent(rows, cols, lda), true, false};
+  ops[1] = {(void*)d.data, 8, sd, (long long)d.pm * d.cn, true, true};  // pad lanes survive
+  int rc = run_batched(routine, ops, batch, stream, res, -1,
+                       [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
+                         return pack_launch(tr, d.m, d.n, (const double*)p[0], lda, sa, (double*)p[1], d.ps,
+                                            d.cn, sd, nb, s);
+                       });
+  if (rc) return rc;
+  return finish(res, 0, 0);
+}
+
+// panel_mat.hpp:164-171: a <- unpacked s; only the m x n interior is read.
+static int unpack_impl(bool batched, pb_dmat src, long long ss, double* a, int lda, long long sa,
+                       int batch, pb_stream stream, pb_result* res) {
+  const char* routine = "unpack_to_colmajor";
+  if (!dmat_shape_ok(src)) return fail(res, routine, 1, 1, "source is not a consistent panel descriptor");
+  if (lda < std::max(1, src.m)) return fail(res, routine, 3, 3, "lda is smaller than m");
+  if (batched) {
+    if (batch < 0) return fail(res, routine, 5, 5, "batch is negative");
+    if (ss < 0 || sa < 0) return fail(res, routine, 6, 6, "a stride is negative");
+  }
+  if (src.m == 0 || src.n == 0 || batch == 0) return finish(res, 0, 0);
+  std::vector<Operand> ops(2);
+  ops[0] = {(void*)src.data, 8, ss, (long long)src.pm * src.cn, true, false};
+  ops[1] = {(void*)a, 8, sa, cm_extent(src.m, src.n, lda), !dense(src.m, lda, sa, src.n, batch), true};
+  int rc = run_batched(routine, ops, batch, stream, res, -1,
+                       [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
+                         return unpack_launch(src.m, src.n, (const double*)p[0], src.ps, src.cn, ss,
+                                              (double*)p[1], lda, sa, nb, s);
+                       });
+  if (rc) return rc;
+  return finish(res, 0, 0);
+}
+
+int pb_pack(char trans, const double* a, int lda, pb_dmat d, pb_result* res) {
+  return pack_impl(false, trans, a, lda, 0, d, 0, 1, nullptr, res);
+}
+int pb_pack_batched(char trans, const double* a, int lda, long long stride_a, pb_dmat d,
+                    long long stride_d, int batch, pb_stream stream, pb_result* res) {
+  return pack_impl(true, trans, a, lda, stride_a, d, stride_d, batch, stream, res);
+}
+int pb_unpack(pb_dmat s, double* a, int lda, pb_result* res) {
+  return unpack_impl(false, s, 0, a, lda, 0, 1, nullptr, res);
+}
+int pb_unpack_batched(pb_dmat s, long long stride_s, double* a, int lda, long long stride_a, int batch,
+                      pb_stream stream, pb_result* res) {
+  return unpack_impl(true, s, stride_s, a, lda, stride_a, batch, stream, res);
+}
+
+// ============================================================== Riccati
+// riccati.hpp:257-373 (RiccatiFusedWork), 402-512 (riccati_run, FusedNative):
+// a batch of independent OCPs with the same (nx, nu, N).
+int pb_riccati_nd_batched(int nx, int nu, int N, pb_dmat m0, long long stride_m0, pb_dmat q,
+                          long long stride_q, pb_dmat g, long long stride_g, pb_dmat f,
+                          long long stride_f, pb_dmat lterm, long long stride_lterm, int* info,
+                          int* stage, int batch, pb_stream stream, pb_result* res) {
+  const char* routine = "riccati";
+  // riccati.hpp:50-52 / 409-412: nx >= 1, nu >= 0, N >= 1 (info -1)
+  if (nx < 1 || nu < 0 || N < 1) return status(res, -1, "dims must satisfy nx >= 1, nu >= 0, N >= 1");
+  const int nt = nx + nu;
+  if (!panel_ok(m0, nt, nt)) return status(res, -4, "m0 panel mismatch");
+  if (!panel_ok(q, nx, nx)) return status(res, -6, "q panel mismatch");
+  if (!panel_ok(g, nt, nx)) return status(res, -8, "g panel mismatch");
+  if (!panel_ok(f, nt, nt)) return status(res, -10, "f panel mismatch");
+  const long long f_len = (long long)f.pm * f.cn;
+  if (stride_f < f_len * N) return status(res, -11, "f stride below N stage factors");
+  if (lterm.data && !panel_ok(lterm, nx, nx)) return status(res, -12, "lterm panel mismatch");
+  if (batch < 0) return status(res, -16, "batch is negative");
+  if (!info && batch > 0) return status(res, -14, "info is null");
+  if (batch == 0) return finish(res, 0, 0);
+  std::vector<Operand> ops(7);
+  ops[0] = {(void*)m0.data, 8, stride_m0, pm_extent(m0), true, false};
+  ops[1] = {(void*)q.data, 8, stride_q, pm_extent(q), true, false};
+  ops[2] = {(void*)g.data, 8, stride_g, pm_extent(g), true, false};
+  ops[3] = {(void*)f.data, 8, stride_f, f_len * N, false, true};
+  ops[4] = {(void*)lterm.data, 8, stride_lterm, lterm.data ? pm_extent(lterm) : 0, true, true};
+  ops[5] = {(void*)info, 4, 1, 1, false, true};
+  ops[6] = {(void*)stage, 4, 1, 1, false, true};
+  int rc = run_batched(routine, ops, batch, stream, res, 3,
+                       [&](const std::vector<void*>& p, int nb, cudaStream_t s) -> cudaError_t {
+                         RiccatiLaunch R;
+                         R.nx = nx; R.nu = nu; R.N = N;
+                         R.m0 = (const double*)p[0]; R.sm0 = stride_m0; R.cnm0 = m0.cn;
+                         R.q = (const double*)p[1]; R.sq = stride_q; R.cnq = q.cn;
+                         R.g = (const double*)p[2]; R.sg = stride_g; R.cng = g.cn;
+                         R.f = (double*)p[3]; R.sf = stride_f; R.cnf = f.cn;
+                         R.lterm = (double*)p[4]; R.sl = stride_lterm; R.cnl = lterm.cn;
+                         R.info = (int*)p[5];
+                         R.stage = (int*)p[6];
+                         R.batch = nb;
+                         return riccati_launch(R, s);
+                       });
+  if (rc) return rc;
+  // flops of the horizon (level3.hpp:479 trmm m n^2; syrk_potrf_nd n^3/3 + n^2 k, :572-573)
+  const long long per_stage = (long long)nt * nx * nx + (long long)nt * nt * nt / 3 + (long long)nt * nt * nx;
+  return finish(res, 0, ((long long)nx * nx * nx / 3 + N * per_stage) * batch);
 }
 
 }  // extern "C"

@@ -221,6 +221,53 @@ for n in (6, 13, 21, 64):
     assert R.trsm_rltn_nd(11, n, 1.5, ob.dmat(d, n, n), ob.dmat(bp, 11, n), ob.dmat(x, 11, n)) == 0
     put(f"chain_nd_{n}", a=ap, c=sp, l=d, b=bp, x=x, nk=[n, k])
 
+# ---- dtrmm: all 16 flag combinations (bench.hpp:548-583 verify recipe shape), alpha 1.5
+for sd in "lr":
+    for ul in "lu":
+        for tr in "nt":
+            for dg in "nu":
+                m, n = 9, 7
+                t = m if sd == "l" else n
+                a = fill(45, t, t)
+                b = fill(46, m, n)
+                d = b.copy(order="F")
+                assert R.dtrmm(sd.encode(), ul.encode(), tr.encode(), dg.encode(), m, n, 1.5, a.ctypes.data, t,
+                               d.ctypes.data, m) == 0
+                put(f"dtrmm_{sd}{ul}{tr}{dg}", a=a, b=b, out=d)
+
+# ---- trmm_rlnn_nd (level3.hpp:446-479), the Riccati stage's first call (riccati.hpp:319)
+for (m, n) in ((11, 7), (13, 16)):
+    A = fill(47, n, n)
+    Bm = fill(48, m, n)
+    ap, bp = ob.pack(A, fill=7.5), ob.pack(Bm, fill=-3.0)
+    d = np.full(ob.panel_len(m, n), 1.25)
+    assert R.trmm_rlnn_nd(m, n, 1.5, ob.dmat(ap, n, n), ob.dmat(bp, m, n), ob.dmat(d, m, n)) == 0
+    put(f"trmm_nd_{m}x{n}", a=ap, b=bp, d0=np.full(ob.panel_len(m, n), 1.25), out=d, mn=[m, n])
+
+# ---- pack / unpack (panel_mat.hpp:141-171), pad lanes untouched
+for (m, n, tr) in ((9, 6, "n"), (9, 6, "t"), (4, 8, "n")):
+    src = fill(49, *((m, n) if tr == "n" else (n, m)))
+    d = np.full(ob.panel_len(m, n), -2.75)
+    R.pack_from_colmajor(tr.encode(), src.ctypes.data, src.shape[0], src.shape[0], src.shape[1], ob.dmat(d, m, n))
+    back = F(np.zeros((m, n)))
+    R.unpack_to_colmajor(ob.dmat(d, m, n), back.ctypes.data, m)
+    put(f"pack_{m}x{n}{tr}", src=src, out=d, back=back)
+
+# ---- Riccati (riccati.hpp): make_ocp_data + RiccatiFusedWork stage factors, riccati_run residuals
+for (nx, nu, N) in ((4, 2, 3), (6, 3, 5), (8, 4, 10)):
+    seed = 1234 + nx
+    a = np.zeros(nx * nx); b = np.zeros(nx * nu); q = np.zeros(nx * nx); r = np.zeros(nu * nu); s_ = np.zeros(nu * nx)
+    R.make_ocp_data(nx, nu, seed, a.ctypes.data, b.ctypes.data, q.ctypes.data, r.ctypes.data, s_.ctypes.data)
+    nt = nx + nu
+    fst = np.zeros(N * nt * nt); lt = np.zeros(nx * nx)
+    import ctypes
+    fs = ctypes.c_int(0)
+    assert R.riccati_fused(nx, nu, N, seed, fst.ctypes.data, lt.ctypes.data, ctypes.byref(fs)) == 0
+    info = ctypes.c_int(0)
+    res = [R.riccati_run(nx, nu, N, impl, seed, ctypes.byref(info)) for impl in (0, 1, 2)]
+    put(f"riccati_{nx}_{nu}_{N}", a=a, b=b, q=q, r=r, s=s_, f=fst, lterm=lt, dims=[nx, nu, N, seed],
+        residual=np.array(res))
+
 # seeded generator check values (matgen.hpp:14-28): Rng(42).uniform() x 8
 put("rng42", u=rng_uniform(42, 8))
 

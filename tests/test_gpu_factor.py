@@ -246,7 +246,9 @@ def test_trsm_rltn_nd_alpha_zero(pb, orc):
     assert pb.trsm_rltn_nd_batched(m, n, 0.0, P(As, n, n), n * n, P(Bs, m, n), L, P(Ds, m, n), L, info, batch).ok()
     assert info.cpu().tolist() == [0, 5, 0]
     out = Ds.cpu().numpy()
-    assert same_bits(out[0], want) and same_bits(out[2], want) and (out[1] == 7.0).all()
+    want7 = np.full(L, 7.0)
+    assert orc.trsm_rltn_nd(m, n, 0.0, dmat(ap, n, n), dmat(bp, m, n), dmat(want7, m, n)) == 0
+    assert same_bits(out[0], want7) and same_bits(out[2], want7) and (out[1] == 7.0).all()
 
 
 def test_dgetrf_host_ipiv_stride_gaps(pb, orc):

@@ -168,3 +168,112 @@ def test_argument_validation_matches_reference(orc):
     assert call("n", "t", 2, 3, 2, 2, 2, 2) == 10
     assert call("n", "n", 2, 2, 2, 2, 2, 1) == 13
     assert call("x", "q", -1, -1, -1, 0, 0, 0) == 1
+
+
+# ---------------------------------------------------------------- round 2: trmm, pack, chain, Riccati
+@pytest.mark.parametrize("case", cases("dtrmm_"))
+def test_golden_dtrmm(orc, case):
+    a, b, out = (F(g(case, x)) for x in "a b out".split())
+    sd, ul, tr, dg = case[-4:]
+    m, n = b.shape
+    d = b.copy(order="F")
+    assert orc.dtrmm(ch(sd), ch(ul), ch(tr), ch(dg), m, n, 1.5, ptr(a), a.shape[0], ptr(d), m) == 0
+    assert same_bits(d, out)
+
+
+@pytest.mark.parametrize("case", cases("trmm_nd_"))
+def test_golden_trmm_rlnn_nd(orc, case):
+    m, n = (int(x) for x in g(case, "mn"))
+    ap, bp, d = g(case, "a").copy(), g(case, "b").copy(), g(case, "d0").copy()
+    assert orc.trmm_rlnn_nd(m, n, 1.5, ob.dmat(ap, n, n), ob.dmat(bp, m, n), ob.dmat(d, m, n)) == 0
+    assert same_bits(d, g(case, "out"))
+    io = bp.copy()  # b aliases d (level3.hpp:443-445)
+    assert orc.trmm_rlnn_nd(m, n, 1.5, ob.dmat(ap, n, n), ob.dmat(io, m, n), ob.dmat(io, m, n)) == 0
+    assert same_bits(ob.unpack(io, m, n), ob.unpack(g(case, "out"), m, n))
+
+
+@pytest.mark.parametrize("case", cases("pack_"))
+def test_golden_pack(case):
+    src, out = F(g(case, "src")), g(case, "out")
+    tr = case[-1]
+    m, n = (src.shape if tr == "n" else src.shape[::-1])
+    d = np.full(ob.panel_len(m, n), -2.75)
+    i = np.arange(m)[:, None]; j = np.arange(n)[None, :]
+    cn = ob.round_up(n, 4)
+    d[(i // 4) * 4 * cn + j * 4 + i % 4] = src if tr == "n" else src.T
+    assert same_bits(d, out)
+    assert same_bits(ob.unpack(out, m, n), F(g(case, "back")))
+
+
+@pytest.mark.parametrize("case", cases("riccati_"))
+def test_golden_riccati_fused(orc, case):
+    """The oracle's composition of the packed stage loop reproduces RiccatiFusedWork bit for bit."""
+    import riccati_ref as rr
+    nx, nu, N, seed = (int(x) for x in g(case, "dims"))
+    nt = nx + nu
+    a = g(case, "a").reshape(nx, nx).T; b = g(case, "b").reshape(nu, nx).T
+    q = g(case, "q").reshape(nx, nx).T; r = g(case, "r").reshape(nu, nu).T; s = g(case, "s").reshape(nx, nu).T
+    m0p, qp, gp = rr.stage_data(a, b, q, r, s)
+    fs, lterm, info, st = rr.fused_oracle(orc, m0p, qp, gp, nx, nu, N)
+    assert info == 0
+    assert same_bits(ob.unpack(lterm, nx, nx), F(g(case, "lterm").reshape(nx, nx).T))
+    want = g(case, "f").reshape(N, nt, nt)
+    for s_ in range(N):
+        got = np.tril(ob.unpack(fs[s_], nt, nt))
+        assert same_bits(F(got), F(want[s_].T))
+    # whole-horizon residual (riccati_run) is tiny for every reference path
+    assert (g(case, "residual") <= 1e-10).all()
+    P = rr.textbook(a, b, q, r, s, N)
+    for s_ in range(N):
+        assert rr.chol_residual(ob.unpack(fs[s_], nt, nt)[nu:, nu:], P[s_]) <= 1e-10
+
+
+@pytest.mark.skipif(not ob.have_ref(), reason="oracle/_ref not built (needs /root/reference)")
+def test_round2_restatements_equal_reference(orc):
+    """dtrmm (16 flag sets), trmm_rlnn_nd, the threaded gemm_nd and chain loops: bit for bit."""
+    R = ob.ref()
+    rng = np.random.default_rng(11)
+    for trial in range(4):
+        m, n = (int(x) for x in rng.integers(1, 30, 2))
+        for sd in "lr":
+            for ul in "lu":
+                for tr in "nt":
+                    for dg in "nu":
+                        t = m if sd == "l" else n
+                        A = F(rng.uniform(-1, 1, (t, t)))
+                        B = F(rng.uniform(-1, 1, (m, n))); b1, b2 = B.copy(order="F"), B.copy(order="F")
+                        i1 = orc.dtrmm(ch(sd), ch(ul), ch(tr), ch(dg), m, n, -0.75, ptr(A), t, ptr(b1), m)
+                        i2 = R.dtrmm(ch(sd), ch(ul), ch(tr), ch(dg), m, n, -0.75, ptr(A), t, ptr(b2), m)
+                        assert i1 == i2 == 0 and same_bits(b1, b2)
+        A = rng.uniform(-1, 1, (n, n)); Bm = rng.uniform(-1, 1, (m, n))
+        ap, bp = ob.pack(A), ob.pack(Bm)
+        d1, d2 = np.full(ob.panel_len(m, n), 3.0), np.full(ob.panel_len(m, n), 3.0)
+        assert orc.trmm_rlnn_nd(m, n, 0.5, ob.dmat(ap, n, n), ob.dmat(bp, m, n), ob.dmat(d1, m, n)) == 0
+        assert R.trmm_rlnn_nd(m, n, 0.5, ob.dmat(ap, n, n), ob.dmat(bp, m, n), ob.dmat(d2, m, n)) == 0
+        assert same_bits(d1, d2)
+    # threaded loops over a small batch
+    s = 12; batch = 9; L = s * s
+    A, B, Cp = (rng.uniform(-1, 1, (batch, L)) for _ in range(3))
+    D1, D2 = np.zeros((batch, L)), np.zeros((batch, L))
+    dm = lambda x: ob.dmat(x, s, s)
+    orc.gemm_nd_batch(b"n", b"t", s, s, s, 1.0, dm(A), L, dm(B), L, 1.0, dm(Cp), L, dm(D1), L, batch, 4)
+    R.gemm_nd_batch(b"n", b"t", s, s, s, 1.0, dm(A), L, dm(B), L, 1.0, dm(Cp), L, dm(D2), L, batch, 4)
+    assert same_bits(D1, D2)
+    ns = (rng.integers(1, 17, 40) * 4).astype(np.int32)
+    offs = np.concatenate([[0], np.cumsum(ns.astype(np.int64) ** 2)[:-1]]).astype(np.int64)
+    tot = int((ns.astype(np.int64) ** 2).sum())
+    for pm in (0, 1):
+        Av = rng.uniform(-1, 1, tot); Bv = rng.uniform(-1, 1, tot)
+        Cv = np.zeros(tot)
+        for n_, o in zip(ns, offs):
+            n_ = int(n_)
+            idx = np.arange(n_)
+            Cv[o + (idx * (n_ + 1) if pm == 0 else (idx // 4) * 4 * n_ + idx * 4 + idx % 4)] = n_
+        outs = []
+        for lib, fn in ((orc, "chain_batch"), (R, "chain_cm_batch" if pm == 0 else "chain_pm_batch")):
+            a_, c_, b_ = Av.copy(), Cv.copy(), Bv.copy(); info = np.full(len(ns), -1, np.int32)
+            args = (ptr(ns), ptr(offs), ptr(a_), ptr(c_), ptr(b_), ptr(info), len(ns), 4)
+            getattr(lib, fn)(*((pm,) + args if fn == "chain_batch" else args))
+            outs.append((c_, b_, info))
+        assert same_bits(outs[0][0], outs[1][0]) and same_bits(outs[0][1], outs[1][1])
+        assert np.array_equal(outs[0][2], outs[1][2]) and (outs[0][2] == 0).all()
