@@ -96,8 +96,9 @@ __global__ void __launch_bounds__(256) getrf_smem_kernel(const __grid_constant__
         __syncwarp();
         for (int i = col + 1 + lane; i < m; i += 32) {
           const double f = A(i, col);
-          if (f != 0.0)
-            for (int c2 = c + 1; c2 < w; ++c2) A(i, c0 + c2) -= f * A(col, c0 + c2);
+          // zero multipliers skip only the rest of the nr = 4 column block
+          for (int c2 = c + 1; c2 < w; ++c2)
+            if (f != 0.0 || c2 > (c | 3)) A(i, c0 + c2) -= f * A(col, c0 + c2);
         }
         __syncwarp();
       }

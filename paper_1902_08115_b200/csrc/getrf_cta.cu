@@ -223,9 +223,11 @@ __global__ void __launch_bounds__(32 * (NU + 1)) getrf_cta_kernel(const __grid_c
           if (act) {
             if (nz) x[q][c] *= inv;
             const double f = x[q][c];
-            if (f != 0.0)
+            // zero multipliers skip only the rest of the nr = 4 column block
+            // (factor.hpp:160-165); the next block takes the plain update
 #pragma unroll
-              for (int c2 = c + 1; c2 < 8; ++c2) x[q][c2] = fma(-f, u[c2], x[q][c2]);
+            for (int c2 = c + 1; c2 < 8; ++c2)
+              if (f != 0.0 || c2 > (c | 3)) x[q][c2] = fma(-f, u[c2], x[q][c2]);
           }
         }
       }

@@ -96,10 +96,12 @@ __global__ void __launch_bounds__(32 * kLuRegWarps, 4) getrf_reg_kernel(const __
     if (!done) {
       if (nz) x[c] *= __drcp_rn(pv);
       const double f = x[c];
-      if (f != 0.0) {
+      // zero multipliers skip only the rest of the reference's nr = 4 column
+      // block (factor.hpp:160-165); later blocks take the plain trailing
+      // update (207-215), where 0 * Inf = NaN
 #pragma unroll
-        for (int j = c + 1; j < N; ++j) x[j] = fma(-f, u[j], x[j]);
-      }
+      for (int j = c + 1; j < N; ++j)
+        if (f != 0.0 || j > (c | 3)) x[j] = fma(-f, u[j], x[j]);
     }
   }
 #pragma unroll

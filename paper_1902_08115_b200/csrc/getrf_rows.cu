@@ -110,16 +110,19 @@ __global__ void __launch_bounds__(32 * NW) getrf_rows_kernel(const __grid_consta
     if (act) {
       if (nz) x[c] *= __drcp_rn(upiv);
       const double f = x[c];
-      if (f != 0.0) {
-        // pivot row pairs loaded next to their use (volatile loads stay in
-        // place): the live set is the row plus one pair, not two rows
+      // zero multipliers are skipped only inside the reference's nr = 4 column
+      // block (factor.hpp:160-165); later blocks get the plain trailing update
+      // (207-215), where 0 * Inf = NaN reaches them
+      const bool fz = f == 0.0;
+      // pivot row pairs loaded next to their use (volatile loads stay in
+      // place): the live set is the row plus one pair, not two rows
 #pragma unroll
-        for (int j = (c + 1) & ~1; j < N; j += 2) {
-          double u0, u1;
-          lds128(urow + 8u * j, u0, u1);
-          if (j >= c + 1) x[j] = fma(-f, u0, x[j]);
-          x[j + 1] = fma(-f, u1, x[j + 1]);
-        }
+      for (int j = (c + 1) & ~1; j < N; j += 2) {
+        if (fz && j + 1 <= (c | 3)) continue;
+        double u0, u1;
+        lds128(urow + 8u * j, u0, u1);
+        if (j >= c + 1 && !(fz && j <= (c | 3))) x[j] = fma(-f, u0, x[j]);
+        x[j + 1] = fma(-f, u1, x[j + 1]);
       }
     }
   }

@@ -101,9 +101,9 @@ __device__ __forceinline__ void named_sync(int id, int count) {
 // round trip on the dependency chain; the lane's own rows follow the same
 // recurrence (the rows of D itself come out bitwise equal to D's entries,
 // the strict upper part of the block is scratch).
-// Slow twin for the rare panels whose pivots are denormal or +inf (where the
-// branch-free rsqrt_nb is not exact): CUDA rsqrt(), rows straight in shared
-// memory, early exit at a failed column.
+// Slow twin for the rare panels whose pivots are denormal, +inf or NaN (where
+// the branch-free rsqrt_nb is not exact): the reference's sqrt and reciprocal,
+// rows straight in shared memory, early exit at a failed column.
 __device__ __noinline__ int cta_factor_panel_exact(uint32_t pan, int RS, int rows, int lane, int gcol0, int n) {
   int f = 0;
   for (int c = 0; c < 8; ++c) {
@@ -113,10 +113,12 @@ __device__ __noinline__ int cta_factor_panel_exact(uint32_t pan, int RS, int row
       f = c + 1;
       break;
     }
-    const double inv = rsqrt(piv);
+    // the reference's s = sqrt(piv), inv = 1 / s (micro_kernel.hpp:315-318): an
+    // Inf pivot gives L_cc = Inf and zeros below, not Inf * 0
+    const double sq = sqrt(piv), inv = 1.0 / sq;
     for (int r = c + lane; r < rows; r += 32) {
       const uint32_t a = pan + 8u * (c * RS + r);
-      sts64(a, r == c ? piv * inv : lds64(a) * inv);
+      sts64(a, r == c ? sq : lds64(a) * inv);
     }
     __syncwarp();
     for (int c2 = c + 1; c2 < 8; ++c2) {

@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_k
   }
 
   const uint32_t buf0 = smem_u32(&colbuf[warp][0][seg * W * RR]);
-  unsigned bad = 0;  // bit c: column c's pivot failed the test
+  unsigned bad = 0;   // bit c: column c's pivot failed the test
+  unsigned infp = 0;  // bit c: column c's pivot is +Inf (L_cc = sqrt(+Inf) = +Inf, not Inf * 0)
 #pragma unroll
   for (int c = 0; c < N; ++c) {
     const uint32_t buf = buf0 + (c & 1) * 32 * RR * 8;
@@ -81,9 +82,10 @@ __global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_k
     for (int c2 = c & ~1; c2 < N; c2 += 2) lds128(buf + 8u * c2, col[c2], col[c2 + 1]);
     const double piv = col[c];  // == x[.][c] on the row c
     bad |= (piv <= 0.0 ? 1u : 0u) << c;
+    infp |= (piv == __longlong_as_double(0x7ff0000000000000LL) ? 1u : 0u) << c;
     double inv = rsqrt_nb(piv);
-    if (__any_sync(0xffffffffu, rsqrt_special(piv)))  // denormal / +inf pivots: exact path
-      inv = rsqrt_special(piv) ? rsqrt(piv) : inv;
+    // denormal / +inf pivots: CUDA's full rsqrt (within 1 ulp of the reference's 1 / sqrt(piv))
+    if (__any_sync(0xffffffffu, rsqrt_special(piv))) inv = rsqrt_special(piv) ? rsqrt(piv) : inv;
 #pragma unroll
     for (int q = 0; q < RR; ++q) {
       x[q][c] *= inv;
@@ -119,6 +121,9 @@ __global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_k
           wp += cs;
         }
       }
+      // +Inf pivots (rare): the diagonal is sqrt(+Inf) = +Inf, not the Inf * 0 in x
+      if ((infp >> r) & 1u && row_ok && r < ncols)
+        rowp(r)[(long long)r * cs] = __longlong_as_double(0x7ff0000000000000LL);
     }
     if (i == 0) P.info[p] = fail ? fail + P.info_offset : 0;
   } else if (live && i == 0) {

@@ -93,6 +93,32 @@ __global__ void __launch_bounds__(256) diag_inv8_kernel(const __grid_constant__ 
 // half-warp.
 __device__ __forceinline__ int ab_idx(int c, int g) { return c * 8 + (g ^ (((c >> 1) & 1) << 2)); }
 
+// Exact 8x8 diagonal-block solve for tiles holding Inf / NaN: substitution in
+// the reference's order (edge_trsm_right, micro_kernel.hpp:330-356), so no
+// structural zero of inv(L_JJ) meets an Inf or NaN of C (0 * Inf = NaN there,
+// not in the reference).  Every lane of a quad solves its row redundantly.
+// Out of line: the fast path keeps its registers.
+__device__ __noinline__ void rlt_tile_exact(double& x0, double& x1, double u00, double u01, double u10, double u11,
+                                            const double* ab, int J, int n, int unit, int lane) {
+  // lane (g, t) holds C(g, 2h), C(g, 2h + 1), C(g, 4 + 2h), C(g, 5 + 2h) with h = t >> 1
+  const int t = lane & 3;
+  double xv[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int src = (lane & ~3) | (((c >> 1) & 1) << 1);  // a lane with h = (c >> 1) & 1
+    xv[c] = __shfl_sync(0xffffffffu, c < 4 ? ((c & 1) ? u01 : u00) : ((c & 1) ? u11 : u10), src);
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    if (8 * J + c >= n) { xv[c] = 0.0; continue; }
+#pragma unroll
+    for (int l = 0; l < c; ++l) xv[c] -= xv[l] * ab[ab_idx(8 * J + l, c)];
+    if (!unit) xv[c] *= 1.0 / ab[ab_idx(8 * J + c, c)];
+  }
+  x0 = t == 0 ? xv[0] : t == 1 ? xv[2] : t == 2 ? xv[4] : xv[6];
+  x1 = t == 0 ? xv[1] : t == 1 ? xv[3] : t == 2 ? xv[5] : xv[7];
+}
+
 // NT > 0: register-resident variant for up to NT column tiles — the solved X
 // stays in registers (A-fragment order, 2 doubles per tile and lane), the
 // tile loops are fully unrolled, and shared memory holds only the staged rows
@@ -221,6 +247,10 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
       acc0 = acc1 = 0.0;
       dmma(acc0, acc1, (t & 1) ? u01 : u00, w0);
       dmma(acc0, acc1, (t & 1) ? u11 : u10, w1);
+      // an Inf / NaN in C or in inv(L_JJ) always leaves a non-finite X: redo
+      // such tiles by substitution (rare; warp-uniform)
+      if (__any_sync(0xffffffffu, !(isfinite(acc0) && isfinite(acc1))))
+        rlt_tile_exact(acc0, acc1, u00, u01, u10, u11, ab, J, n, L.unit, lane);
     }
     if (rok && ca < n) D[xo(ldd, r, ca)] = acc0;
     if (rok && cb < n) D[xo(ldd, r, cb)] = acc1;

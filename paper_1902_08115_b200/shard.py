@@ -40,3 +40,32 @@ def cost_balanced_shard(costs: Sequence[float], world: int, rank: int) -> tuple[
         cuts.append(len(costs))
     cuts.append(len(costs))
     return cuts[rank], cuts[rank + 1]
+
+
+def shard_of(batch: int, world: int, rank: int, costs: Sequence[float] | None = None) -> tuple[int, int]:
+    """The slice of one host-generated batch that `rank` computes: contiguous equal slices,
+    or equal-cost slices when per-problem `costs` are given."""
+    if costs is not None:
+        if len(costs) != batch:
+            raise ValueError("costs must have one entry per problem")
+        return cost_balanced_shard(costs, world, rank)
+    return contiguous_shard(batch, world, rank)
+
+
+def gather_slices(local, lo: int, hi: int, world: int, rank: int, root: int = 0):
+    """Collects every rank's [lo, hi) result slice (numpy, problem-major) on `root` in problem
+    order and returns the concatenation there (None elsewhere).  Host-side only: the data path
+    itself has no collective; this is the optional D2H gather of §8e for parity checks."""
+    import numpy as np
+    if world == 1:
+        return local
+    import torch.distributed as dist
+    objs = [None] * world if rank == root else None
+    dist.gather_object((lo, hi, local), objs, dst=root)
+    if rank != root:
+        return None
+    objs.sort(key=lambda o: o[0])
+    for a, b in zip(objs, objs[1:]):
+        if a[1] != b[0]:
+            raise RuntimeError("shards do not tile the batch")
+    return np.concatenate([o[2] for o in objs])

@@ -93,7 +93,8 @@ def test_trmm_rlnn_nd(pb, orc, cuda):
     got = dD.cpu().numpy()
     for p in range(batch):
         w = np.zeros(Lb)
-        orc.trmm_rlnn_nd(m, n, 1.0, ob.dmat(As[p].copy(), n, n), ob.dmat(Bs[p].copy(), m, n), ob.dmat(w, m, n))
+        ap_, bp_ = As[p].copy(), Bs[p].copy()  # keep the buffers alive: a Dmat holds a raw address
+        orc.trmm_rlnn_nd(m, n, 1.0, ob.dmat(ap_, n, n), ob.dmat(bp_, m, n), ob.dmat(w, m, n))
         assert rel_frob(ob.unpack(got[p], m, n), ob.unpack(w, m, n)) <= tol(n)
 
 
