@@ -99,12 +99,39 @@ __global__ void k(double* out, long long* cyc, double x0) {
   }
   t1 = clock64(); cyc[9] = t1 - t0;
   double acc = 0; for (int j = 0; j < 8; ++j) acc += e[j][0] + e[j][1];
+  // rsqrt_nb chain (rsqrt.approx.ftz.f64 + one third-order Newton step, common.cuh)
+  t0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < 256; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double yy;
+      asm("rsqrt.approx.ftz.f64 %0, %1;\n" : "=d"(yy) : "d"(x));
+      const double ee = fma(-x, yy * yy, 1.0);
+      const double cc = fma(ee, 0.375, 0.5);
+      x = fma(cc, yy * ee, yy) + 0.5;
+    }
+  }
+  t1 = clock64(); cyc[10] = t1 - t0;
+  // shared-memory load chain (pointer chase through a 32-entry ring)
+  __shared__ int ring[64];
+  ring[threadIdx.x] = (threadIdx.x + 1) & 31;
+  __syncwarp();
+  int pidx = threadIdx.x;
+  t0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < 256; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) pidx = ((volatile int*)ring)[pidx];
+  }
+  t1 = clock64(); cyc[11] = t1 - t0;
+  acc += pidx;
   out[threadIdx.x] = x + s + d0 + d1 + acc;
 }
 int main() {
   double* o; long long* c; cudaMalloc(&o, 8 * 32); cudaMallocManaged(&c, 8 * 16);
   k<<<1, 32>>>(o, c, 1.5); cudaDeviceSynchronize();
   k<<<1, 32>>>(o, c, 1.5); cudaDeviceSynchronize();
-  const char* nm[] = {"dfma", "dmul", "rsqrt(double)", "rsqrtf+2NR", "sqrt(double)", "1/x", "shfl", "dadd", "dmma dep", "dmma 8 indep"};
-  for (int i = 0; i < 10; ++i) printf("%-16s %6.1f cycles/op\n", nm[i], c[i] / 2048.0);
+  const char* nm[] = {"dfma", "dmul", "rsqrt(double)", "rsqrtf+2NR", "sqrt(double)", "1/x", "shfl", "dadd", "dmma dep", "dmma 8 indep", "rsqrt_nb", "lds chain"};
+  for (int i = 0; i < 12; ++i) printf("%-16s %6.1f cycles/op\n", nm[i], c[i] / 2048.0);
 }

@@ -8,7 +8,7 @@
 #include <vector>
 
 namespace pbg {
-int num_sms() { return 164; }
+
 }
 
 __global__ void make_spd(double* a, int n, int batch) {
