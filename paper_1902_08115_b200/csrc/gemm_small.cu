@@ -332,8 +332,8 @@ static cudaError_t small_t(SmallArgs& P, cudaStream_t st) {
 
 // ---------------------------------------------------------------------------
 // Column-major NN, square packed problems (m = n = k = lda = ldb = ldc = s <= 64,
-// stride s*s): config 1's shape.  Same row-tile split as gemm_mid_kernel, one
-// problem per CTA iteration on a 2-stage ring; A, B and C arrive as ONE 2-D
+// stride s*s): config 1's shape.  One problem per CTA iteration on a 2-stage
+// ring (one CTA per SM: 2 x 104 KB at s = 64); A, B and C arrive as ONE 2-D
 // TMA tensor copy each whose box is 4 rows taller than the problem (the rows
 // past s are the out-of-bounds zero fill), which gives the column stride
 // s + 4 = 4 mod 16 doubles: conflict-free fragment loads for both operands.
@@ -348,13 +348,23 @@ struct CmArgs {
   int s;
 };
 
-#ifndef CM_SPLIT
-#define CM_SPLIT 2
-#endif
+// Warp blocks: warp w owns RI x RJ tiles of 8x8 (row tiles I0..I0+RI-1, column
+// tiles J0..J0+RJ-1) — RI + RJ fragment loads feed RI * RJ independent DMMA
+// chains per k step, and the next step's fragments are loaded under the
+// current step's DMMAs (register double buffer).
+template <int T> struct CmShape;
+template <> struct CmShape<4> { static constexpr int RI = 1, RJ = 2; };
+template <> struct CmShape<5> { static constexpr int RI = 1, RJ = 5; };
+template <> struct CmShape<6> { static constexpr int RI = 1, RJ = 3; };
+template <> struct CmShape<7> { static constexpr int RI = 1, RJ = 7; };
+template <> struct CmShape<8> { static constexpr int RI = 2, RJ = 4; };
+template <int T> __host__ __device__ constexpr int cm_warps() { return (T / CmShape<T>::RI) * (T / CmShape<T>::RJ); }
+
 template <int T>
-__global__ void __launch_bounds__(32 * T * CM_SPLIT) gemm_cm_kernel(const __grid_constant__ CmArgs P) {
+__global__ void __launch_bounds__(32 * cm_warps<T>()) gemm_cm_kernel(const __grid_constant__ CmArgs P) {
   extern __shared__ __align__(1024) double sm[];
   __shared__ __align__(8) uint64_t full[2];
+  constexpr int RI = CmShape<T>::RI, RJ = CmShape<T>::RJ, NWR = T / RI;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int s = P.s, S = s + CM_PAD, ops = S * s;  // doubles per staged operand
   const bool use_c = P.beta != 0.0;
@@ -381,6 +391,7 @@ __global__ void __launch_bounds__(32 * T * CM_SPLIT) gemm_cm_kernel(const __grid
     tma3(a + 8u * ops, &P.tb, (int)prob, &full[slot]);
     if (use_c) tma3(a + 16u * ops, &P.tc, (int)prob, &full[slot]);
   };
+  const int I0 = (warp % NWR) * RI, J0 = (warp / NWR) * RJ;
   int it = 0;
   long long prob = blockIdx.x;
   if (tid == 0 && prob < P.batch) issue(prob, 0);
@@ -393,36 +404,48 @@ __global__ void __launch_bounds__(32 * T * CM_SPLIT) gemm_cm_kernel(const __grid
     }
     mbar_wait(&full[slot], (it >> 1) & 1);
     const uint32_t A = slot_addr(slot), B = A + 8u * ops, C = B + 8u * ops;
-    // CM_SPLIT warps per row tile, each owning T / CM_SPLIT column tiles
-    constexpr int TJ = (T + CM_SPLIT - 1) / CM_SPLIT;
-    const int I = warp % T, J0 = (warp / T) * TJ;
-    const int nj = min(TJ, T - J0);  // warp-uniform (odd T: the last split owns fewer tiles)
-    double acc[TJ][2];
+    // A(8I+g, l+t) at column l+t, row 8I+g; B(l+t, 8J+g) at column 8J+g, row l+t
+    const uint32_t fa0 = A + 8u * (t * S + 8 * I0 + g), fb0 = B + 8u * ((8 * J0 + g) * S + t);
+    double acc[RI][RJ][2];
 #pragma unroll
-    for (int J = 0; J < TJ; ++J) acc[J][0] = acc[J][1] = 0.0;
-    // rows past s are the zero fill; columns past s (s % 8 != 0) read the next operand and feed discarded outputs
-    for (int l0 = 0; l0 < s; l0 += 4) {
-      const double fa = lds64(A + 8u * ((l0 + t) * S + 8 * I + g));  // A(8I+g, l0+t)
-      double fb[TJ];
+    for (int i = 0; i < RI; ++i)
 #pragma unroll
-      for (int J = 0; J < TJ; ++J)
-        fb[J] = J < nj ? lds64(B + 8u * ((8 * (J0 + J) + g) * S + l0 + t)) : 0.0;  // B(l0+t, 8J+g)
+      for (int j = 0; j < RJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double a0[RI], b0[RJ], a1[RI], b1[RJ];
+    auto load = [&](int l0, double (&fa)[RI], double (&fb)[RJ]) {
 #pragma unroll
-      for (int J = 0; J < TJ; ++J)
-        if (J < nj) dmma(acc[J][0], acc[J][1], fa, fb[J]);
+      for (int i = 0; i < RI; ++i) fa[i] = lds64(fa0 + 8u * (l0 * S + 8 * i));
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) fb[j] = lds64(fb0 + 8u * (l0 + 8 * S * j));
+    };
+    auto mma = [&](const double (&fa)[RI], const double (&fb)[RJ]) {
+#pragma unroll
+      for (int i = 0; i < RI; ++i)
+#pragma unroll
+        for (int j = 0; j < RJ; ++j) dmma(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    };
+    // s % 8 == 0: every tile is inside the problem, s / 4 k steps (even)
+    load(0, a0, b0);
+    int l0 = 0;
+    for (; l0 + 8 <= s; l0 += 8) {
+      load(l0 + 4, a1, b1);
+      mma(a0, b0);
+      if (l0 + 8 < s) load(l0 + 8, a0, b0);
+      mma(a1, b1);
     }
+    if (l0 < s) mma(a0, b0);  // (s % 8 == 4: not reached on this path)
     __syncwarp();
 #pragma unroll
-    for (int J = 0; J < TJ; ++J)
+    for (int i = 0; i < RI; ++i)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int r = 8 * I + g, c = 8 * (J0 + J) + 2 * t + e;
-        if (J < nj && r < s && c < s) {
+      for (int j = 0; j < RJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * (I0 + i) + g, c = 8 * (J0 + j) + 2 * t + e;
           const uint32_t off = C + 8u * (c * S + r);
-          sts64(off, use_c ? fma(P.alpha, acc[J][e], P.beta * lds64(off)) : P.alpha * acc[J][e]);
+          sts64(off, use_c ? fma(P.alpha, acc[i][j][e], P.beta * lds64(off)) : P.alpha * acc[i][j][e]);
         }
-      }
-    fence_proxy_async();
+    fence_proxy_async();  // every writer fences before the barrier that precedes the async-proxy store
     __syncthreads();
     if (tid == 0) {
       asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
@@ -488,7 +511,7 @@ cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b
       cudaError_t e = smem_attr((const void*)gemm_cm_kernel<TV>, 220 * 1024);                            \
       if (e != cudaSuccess) return e;                                                                    \
     }                                                                                                    \
-    gemm_cm_kernel<TV><<<grid, 32 * TV * CM_SPLIT, smem, st>>>(P);                                                  \
+    gemm_cm_kernel<TV><<<grid, 32 * cm_warps<TV>(), smem, st>>>(P);                                      \
     return cudaGetLastError();                                                                           \
   }
   switch (s / 8) {
