@@ -126,44 +126,64 @@ __global__ void __launch_bounds__(32 * SM_WARPS) gemm_small_kernel(const __grid_
 }
 
 // s = 4: a problem is one 4x4 panel (element (i, l) at l*4 + i), 128 bytes per
-// operand.  One thread owns one problem: 16-byte streaming loads of A, B (and
-// C), 64 FMAs in registers, 16-byte stores — the problem is pure HBM traffic
-// and needs no shared memory or tensor cores.
-__global__ void __launch_bounds__(256) gemm_tiny4_kernel(const __grid_constant__ SmallArgs P) {
-  const long long p = (long long)blockIdx.x * 256 + threadIdx.x;
-  if (p >= P.batch) return;
-  const double2* A = reinterpret_cast<const double2*>(P.a + p * 16);
-  const double2* B = reinterpret_cast<const double2*>(P.b + p * 16);
-  double a[16], b[16];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const double2 va = __ldcs(A + u), vb = __ldcs(B + u);
-    a[2 * u] = va.x; a[2 * u + 1] = va.y;
-    b[2 * u] = vb.x; b[2 * u + 1] = vb.y;
-  }
-  double c[16];
+// operand; the problem is pure HBM traffic.  A warp owns 32 consecutive
+// problems: each operand's 4 KB arrive as 8 fully coalesced 512-byte warp
+// loads (all three operands in flight at once), are transposed through a
+// per-warp shared buffer (element e of problem p at e*33 + p: conflict-free
+// both ways) so that each lane holds its own problem, 64 FMAs in registers,
+// and D leaves through the same buffer as coalesced 512-byte stores.
+constexpr int kTinyWarps = 8;
+__global__ void __launch_bounds__(32 * kTinyWarps) gemm_tiny4_kernel(const __grid_constant__ SmallArgs P) {
+  __shared__ double tb[kTinyWarps][16 * 33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long p0 = ((long long)blockIdx.x * kTinyWarps + warp) * 32;
+  if (p0 >= P.batch) return;
+  const int np = (int)min(32LL, P.batch - p0);  // problems of this warp
   const bool use_c = P.beta != 0.0;
-  if (use_c) {
-    const double2* C = reinterpret_cast<const double2*>(P.c + p * 16);
+  double* buf = tb[warp];
+  // coalesced loads: iteration i, lane L -> doubles 64 i + 2 L (+1) of the warp's 512
+  double2 va[8], vb[8], vc[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const double2 v = __ldcs(C + u);
-      c[2 * u] = v.x; c[2 * u + 1] = v.y;
-    }
+  for (int i = 0; i < 8; ++i) {
+    const int pp = 4 * i + (lane >> 3);
+    const long long off = p0 * 16 + 64 * i + 2 * lane;
+    const bool ok = pp < np;
+    va[i] = ok ? __ldcs(reinterpret_cast<const double2*>(P.a + off)) : make_double2(0.0, 0.0);
+    vb[i] = ok ? __ldcs(reinterpret_cast<const double2*>(P.b + off)) : make_double2(0.0, 0.0);
+    vc[i] = ok && use_c ? __ldcs(reinterpret_cast<const double2*>(P.c + off)) : make_double2(0.0, 0.0);
   }
-  double2* D = reinterpret_cast<double2*>(P.d + p * 16);
+  auto transpose_in = [&](const double2 (&v)[8], double (&x)[16]) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {    // column j of D = row j of B
-    double out[4];
+    for (int i = 0; i < 8; ++i) {
+      const int pp = 4 * i + (lane >> 3), e = 2 * (lane & 7);
+      buf[e * 33 + pp] = v[i].x;
+      buf[(e + 1) * 33 + pp] = v[i].y;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) x[e] = buf[e * 33 + lane];
+    __syncwarp();
+  };
+  double a[16], b[16], c[16];
+  transpose_in(va, a);
+  transpose_in(vb, b);
+  if (use_c) transpose_in(vc, c);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)      // column j of D = row j of B
 #pragma unroll
     for (int i = 0; i < 4; ++i) {  // D(i, j) = sum_l A(i, l) B(j, l)
       double acc = 0.0;
 #pragma unroll
       for (int l = 0; l < 4; ++l) acc = fma(a[l * 4 + i], b[l * 4 + j], acc);
-      out[i] = use_c ? fma(P.alpha, acc, P.beta * c[j * 4 + i]) : P.alpha * acc;
+      buf[(j * 4 + i) * 33 + lane] = use_c ? fma(P.alpha, acc, P.beta * c[j * 4 + i]) : P.alpha * acc;
     }
-    __stcs(D + 2 * j, make_double2(out[0], out[1]));
-    __stcs(D + 2 * j + 1, make_double2(out[2], out[3]));
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int pp = 4 * i + (lane >> 3), e = 2 * (lane & 7);
+    if (pp < np)
+      __stcs(reinterpret_cast<double2*>(P.d + p0 * 16 + 64 * i + 2 * lane),
+             make_double2(buf[e * 33 + pp], buf[(e + 1) * 33 + pp]));
   }
 }
 
@@ -544,7 +564,7 @@ cudaError_t gemm_small_launch(int s, double alpha, const double* a, const double
   P.G = std::max(1, 2048 / (s * s));
   P.nchunks = (int)((batch + P.G - 1) / P.G);
   if (s == 4) {
-    gemm_tiny4_kernel<<<(unsigned)((batch + 255) / 256), 256, 0, st>>>(P);
+    gemm_tiny4_kernel<<<(unsigned)((batch + 32 * kTinyWarps - 1) / (32 * kTinyWarps)), 32 * kTinyWarps, 0, st>>>(P);
     return cudaGetLastError();
   }
   if (s >= 28) return mid_launch(P, st);  // measured: ahead of the chunked kernel from s = 28
