@@ -491,20 +491,20 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       if (lane == 0) { PB_STAMP(4 + 2 * k) }
       const int RS = cta_pstride(T, k), rows = 8 * (TT - k);
       if (streamed || P.tma) mbar_wait(&sh_bar[k], 0);
-#ifdef PB_PANEL_REDUNDANT
-      const int f = cta_factor_panel<R>(sbase + 8u * cta_pbase(T, k), RS, rows, lane, 8 * k, n);
-#else
-      // rows per lane follow the panel's height (fewer predicated-off rows in late panels)
+      // from n = 72 on the diagonal block is factored redundantly in every lane
+      // (measured: n = 128 0.497 -> 0.471 ms, 256 -1.5 %; no change below); below
+      // that, rows per lane follow the panel's height (fewer predicated-off rows)
       const uint32_t pk = sbase + 8u * cta_pbase(T, k), cbuf = smem_u32(&sh_col[0][0]);
       int f;
-      if constexpr (R > 1) {
+      if constexpr (T >= 9) {
+        f = cta_factor_panel<R>(pk, RS, rows, lane, 8 * k, n);  // (rows-following measured slower here)
+      } else if constexpr (R > 1) {
         if (rows <= 32) f = cta_factor_panel_bc<1>(pk, RS, rows, lane, 8 * k, n, cbuf);
         else if (R > 2 && rows <= 64) f = cta_factor_panel_bc<(R > 2 ? 2 : R)>(pk, RS, rows, lane, 8 * k, n, cbuf);
         else f = cta_factor_panel_bc<R>(pk, RS, rows, lane, 8 * k, n, cbuf);
       } else {
         f = cta_factor_panel_bc<R>(pk, RS, rows, lane, 8 * k, n, cbuf);
       }
-#endif
       if (f && lane == 0) sh_fail = 8 * k + f;
       if (lane == 0) { PB_STAMP(5 + 2 * k) }
       named_sync(1, NTH);  // panel k published (or the failure flag)
