@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <vector>
 
@@ -120,6 +121,15 @@ cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ chain (cfg 5)
+// PBGPU_CHAIN_UNFUSED=1: column-major small orders as syrk -> potrf launches (A/B only)
+static bool chain_unfused() {
+  static const bool v = [] {
+    const char* e = getenv("PBGPU_CHAIN_UNFUSED");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
   if (L.batch <= 0) return cudaSuccess;
   mempool_keep();
@@ -173,9 +183,13 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       int* bn = d_n + b0;
       int* binfo = d_info + b0;
       long long* boff = d_off + b0;
-      if (!L.pm) {
+      if (!L.pm && (nmax <= 32 || chain_unfused())) {
+        // register-resident Cholesky for the smallest orders: syrk first, then potrf_reg
         e = syrk_lower_cta_launch(L.C, boff, bn, L.A, nmax, 0, binfo, bs, s);
         if (e == cudaSuccess) e = potrf_cta_launch(L.C, 0, boff, bn, 0, nmax, 0, 0, 0, binfo, 0, 0, bs, s);
+      } else if (!L.pm) {
+        // one kernel: S = C + A A^T (lower) formed in shared memory, factored there, written once
+        e = syrk_potrf_cta_launch(L.C, 0, boff, bn, 0, L.C, 0, 0, L.A, L.A, 0, 1, 0, nmax, 0, 0, binfo, bs, s);
       } else {
         e = syrk_potrf_cta_launch(L.C, 0, boff, bn, 0, L.C, 0, 0, L.A, L.A, 0, 1, 0, nmax, 1, 1, binfo, bs, s);
       }

@@ -93,30 +93,26 @@ __global__ void __launch_bounds__(256) diag_inv8_kernel(const __grid_constant__ 
 // half-warp.
 __device__ __forceinline__ int ab_idx(int c, int g) { return c * 8 + (g ^ (((c >> 1) & 1) << 2)); }
 
-// Exact 8x8 diagonal-block solve for tiles holding Inf / NaN: substitution in
-// the reference's order (edge_trsm_right, micro_kernel.hpp:330-356), so no
-// structural zero of inv(L_JJ) meets an Inf or NaN of C (0 * Inf = NaN there,
-// not in the reference).  Every lane of a quad solves its row redundantly.
-// Out of line: the fast path keeps its registers.
-__device__ __noinline__ void rlt_tile_exact(double& x0, double& x1, double u00, double u01, double u10, double u11,
-                                            const double* ab, int J, int n, int unit, int lane) {
-  // lane (g, t) holds C(g, 2h), C(g, 2h + 1), C(g, 4 + 2h), C(g, 5 + 2h) with h = t >> 1
-  const int t = lane & 3;
-  double xv[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int src = (lane & ~3) | (((c >> 1) & 1) << 1);  // a lane with h = (c >> 1) & 1
-    xv[c] = __shfl_sync(0xffffffffu, c < 4 ? ((c & 1) ? u01 : u00) : ((c & 1) ? u11 : u10), src);
+// Exact redo of one warp's 8 rows when its fast solve met an Inf / NaN (rare):
+// substitution in the reference's order (edge_trsm_right, micro_kernel.hpp:
+// 330-356) straight from B, which the fast path leaves untouched until its
+// final store — so no structural zero of inv(L_JJ) meets an Inf or NaN
+// (0 * Inf = NaN there, not in the reference).  Lane g (t == 0) owns row g.
+template <int PM>
+__device__ __noinline__ void rlt_rows_exact(const TrsmLaunch& L, const double* A, const double* B, double* D,
+                                            long long lda, long long ldb, long long ldd, int n, int m, int r0,
+                                            int lane) {
+  const int r = r0 + (lane >> 2);
+  if ((lane & 3) != 0 || r >= m) return;
+  auto xo = [&](long long ld, int rr, int cc) -> long long {
+    return (!PM && L.twin) ? (long long)cc + (long long)rr * ld : rlt_off<PM>(ld, rr, cc);
+  };
+  for (int c = 0; c < n; ++c) {
+    double x = L.alpha * B[xo(ldb, r, c)];
+    for (int l = 0; l < c; ++l) x -= D[xo(ldd, r, l)] * A[rlt_off<PM>(lda, c, l)];
+    if (!L.unit) x *= 1.0 / A[rlt_off<PM>(lda, c, c)];
+    D[xo(ldd, r, c)] = x;
   }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    if (8 * J + c >= n) { xv[c] = 0.0; continue; }
-#pragma unroll
-    for (int l = 0; l < c; ++l) xv[c] -= xv[l] * ab[ab_idx(8 * J + l, c)];
-    if (!unit) xv[c] *= 1.0 / ab[ab_idx(8 * J + c, c)];
-  }
-  x0 = t == 0 ? xv[0] : t == 1 ? xv[2] : t == 2 ? xv[4] : xv[6];
-  x1 = t == 0 ? xv[1] : t == 1 ? xv[3] : t == 2 ? xv[5] : xv[7];
 }
 
 // NT > 0: register-resident variant for up to NT column tiles — the solved X
@@ -124,7 +120,7 @@ __device__ __noinline__ void rlt_tile_exact(double& x0, double& x1, double u00, 
 // tile loops are fully unrolled, and shared memory holds only the staged rows
 // of A, so residency is no longer bounded by 8 rows x n of X per warp.
 template <int PM, int NT>
-__global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_constant__ RltArgs R) {
+__global__ void __launch_bounds__(32 * kRltWarps, PM && NT >= 28 ? 3 : 1) trsm_rlt_kernel(const __grid_constant__ RltArgs R) {
   extern __shared__ __align__(16) double sm_all[];
   const TrsmLaunch& L = R.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, tid = threadIdx.x;
@@ -192,6 +188,7 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
   auto xo = [&](long long ld, int rr, int cc) -> long long {
     return (!PM && L.twin) ? (long long)cc + (long long)rr * ld : rlt_off<PM>(ld, rr, cc);
   };
+  bool bad = false;  // this lane saw a non-finite X
   double nb0 = (rok && 2 * t < n) ? B[xo(ldb, r, 2 * t)] : 0.0;
   double nb1 = (rok && 2 * t + 1 < n) ? B[xo(ldb, r, 2 * t + 1)] : 0.0;
 #pragma unroll
@@ -247,13 +244,9 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
       acc0 = acc1 = 0.0;
       dmma(acc0, acc1, (t & 1) ? u01 : u00, w0);
       dmma(acc0, acc1, (t & 1) ? u11 : u10, w1);
-      // an Inf / NaN in C or in inv(L_JJ) always leaves a non-finite X: redo
-      // such tiles by substitution (rare; warp-uniform)
-      if (__any_sync(0xffffffffu, !(isfinite(acc0) && isfinite(acc1))))
-        rlt_tile_exact(acc0, acc1, u00, u01, u10, u11, ab, J, n, L.unit, lane);
+      // an Inf / NaN in C or in inv(L_JJ) always leaves a non-finite X
+      bad |= !(isfinite(acc0) && isfinite(acc1));
     }
-    if (rok && ca < n) D[xo(ldd, r, ca)] = acc0;
-    if (rok && cb < n) D[xo(ldd, r, cb)] = acc1;
     // ---- re-lay as A fragments: kk = 0 needs column t, kk = 1 column 4 + t ----
     const int src0 = (lane & ~3) | (t >> 1), src1 = (lane & ~3) | (2 + (t >> 1));
     const double v00 = __shfl_sync(0xffffffffu, acc0, src0), v01 = __shfl_sync(0xffffffffu, acc1, src0);
@@ -268,6 +261,28 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     }
   }
   cp_async_wait_all();
+  // D is written only now (B, which it may alias, is intact until here): the
+  // fast result, or — when a tile met an Inf / NaN — the exact redo of the rows
+  if (__any_sync(0xffffffffu, bad)) {
+    rlt_rows_exact<PM>(L, A, B, D, lda, ldb, ldd, n, m, rb * 8, lane);
+  } else {
+    // lane (g, t) holds X(r, 8J + t) and X(r, 8J + 4 + t) (A-fragment order)
+#pragma unroll
+    for (int J = 0; J < (REG ? NT : 1 << 30); ++J) {
+      if (J >= nt) break;
+      double v0, v1;
+      if constexpr (REG) {
+        v0 = xr[REG ? J : 0][0];
+        v1 = xr[REG ? J : 0][1];
+      } else {
+        v0 = lds64(xs + 8u * ((2 * J) * 32 + lane));
+        v1 = lds64(xs + 8u * ((2 * J + 1) * 32 + lane));
+      }
+      const int c0 = 8 * J + t, c1 = c0 + 4;
+      if (rok && c0 < n) D[xo(ldd, r, c0)] = v0;
+      if (rok && c1 < n) D[xo(ldd, r, c1)] = v1;
+    }
+  }
   if (rb == 0 && lane == 0 && L.info && !L.skip_nonzero) L.info[p] = 0;
 }
 
