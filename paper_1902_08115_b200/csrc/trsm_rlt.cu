@@ -120,7 +120,7 @@ __device__ __noinline__ void rlt_rows_exact(const TrsmLaunch& L, const double* A
 // tile loops are fully unrolled, and shared memory holds only the staged rows
 // of A, so residency is no longer bounded by 8 rows x n of X per warp.
 template <int PM, int NT>
-__global__ void __launch_bounds__(32 * kRltWarps, PM && NT >= 28 ? 3 : 1) trsm_rlt_kernel(const __grid_constant__ RltArgs R) {
+__global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_constant__ RltArgs R) {
   extern __shared__ __align__(16) double sm_all[];
   const TrsmLaunch& L = R.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, tid = threadIdx.x;
