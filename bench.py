@@ -606,7 +606,8 @@ def series_chain(S: Series):
         def setup():
             C.copy_(C0); B.copy_(B0)
 
-        ms = _median_ms(lambda: pb.chain_vbatched(layout, dn, doff, A, C, B, info, batch, 256, stream=stream),
+        # n / offset passed as host arrays: the split by order is planned without a device round trip
+        ms = _median_ms(lambda: pb.chain_vbatched(layout, ns, offs, A, C, B, info, batch, 256, stream=stream),
                         stream, reps=2, setup=setup)
         assert int(info.abs().sum()) == 0
         e = {"gflops": round(fl_p.sum() / ms / 1e6, 1), "ms": round(ms, 3), "roofline_frac": round(roof * 1e3 / ms, 3)}

@@ -130,8 +130,12 @@ int pb_syrk_potrf_nd_batched(int n, int k, pb_dmat a, long long stride_a, pb_dma
  *                               dtrsm('r','l','t','n') X L^T = B  (X over B)
  *   layout 'P' (panel-major):   syrk_potrf_nd(n, n, A, A, C, C);
  *                               trsm_rltn_nd(n, n, 1, C, B, B)
- * info[p] = 0, or the failing pivot of the Cholesky step.  n, offset and info
- * are in the same memory kind as the matrices; max_n bounds n[p]. */
+ * info[p] = 0, or the failing pivot of the Cholesky step; max_n bounds n[p].
+ * Memory kinds: A, C, B and info all on the device (asynchronous on `stream`;
+ * with device n / offset the split by order costs one device -> host copy and
+ * a stream synchronisation), n / offset on the HOST with device matrices
+ * (asynchronous, no synchronisation), or everything on the host (staged
+ * through the device, returns when done; the caller's riccati-style buffers). */
 int pb_chain_vbatched(char layout, const int* n, const long long* offset, double* A, double* C,
                       double* B, int* info, int batch, int max_n, pb_stream stream,
                       pb_result* res);

@@ -134,15 +134,21 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
   if (L.batch <= 0) return cudaSuccess;
   mempool_keep();
   cudaError_t e;
-  // The split by order is planned on the host.
+  // The split by order is planned on the host: from the caller's host copies of
+  // n / offset when given (no synchronisation), else from a device -> host copy.
   std::vector<int> nv(L.batch);
   std::vector<long long> ov(L.batch);
-  if ((e = cudaMemcpyAsync(nv.data(), L.n, sizeof(int) * L.batch, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-    return e;
-  if ((e = cudaMemcpyAsync(ov.data(), L.offset, sizeof(long long) * L.batch, cudaMemcpyDeviceToHost, s)) !=
-      cudaSuccess)
-    return e;
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  if (L.n_host && L.offset_host) {
+    std::copy(L.n_host, L.n_host + L.batch, nv.begin());
+    std::copy(L.offset_host, L.offset_host + L.batch, ov.begin());
+  } else {
+    if ((e = cudaMemcpyAsync(nv.data(), L.n, sizeof(int) * L.batch, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return e;
+    if ((e = cudaMemcpyAsync(ov.data(), L.offset, sizeof(long long) * L.batch, cudaMemcpyDeviceToHost, s)) !=
+        cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  }
   std::vector<int> small;
   std::map<int, std::vector<int>> big;
   int nsmall_max = 0;

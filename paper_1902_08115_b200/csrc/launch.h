@@ -189,8 +189,10 @@ cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s);
 // Variable-size chain (config 5).  layout 0 = column-major, 1 = panel-major.
 struct ChainLaunch {
   int pm = 0;
-  const int* n = nullptr;
+  const int* n = nullptr;               // device arrays (always)
   const long long* offset = nullptr;
+  const int* n_host = nullptr;          // optional host copies: the split is planned
+  const long long* offset_host = nullptr;  // without a device -> host round trip
   double *A = nullptr, *C = nullptr, *B = nullptr;
   int* info = nullptr;
   int batch = 0, max_n = 0;

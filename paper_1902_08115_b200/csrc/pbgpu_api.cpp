@@ -973,19 +973,71 @@ int pb_chain_vbatched(char layout, const int* n, const long long* offset, double
   if (max_n < 0) return fail(res, routine, 10, 10, "max_n is negative");
   if (batch == 0) return finish(res, 0, 0);
   if (!device_ok()) return status(res, PB_INFO_NO_DEVICE, "no CUDA device: pbgpu has no CPU path");
-  Kind k = kind_of(A);
-  if (k != K_DEVICE || kind_of(C) != K_DEVICE || kind_of(B) != K_DEVICE || kind_of(n) != K_DEVICE ||
-      kind_of(offset) != K_DEVICE || kind_of(info) != K_DEVICE)
-    return status(res, PB_INFO_UNSUPPORTED, "pb_chain_vbatched takes device pointers");
+  // Memory kinds: everything on the device (asynchronous; the split by order costs
+  // one device -> host copy of n / offset), n / offset on the host with the
+  // matrices on the device (asynchronous, no synchronisation), or everything on
+  // the host (staged through the device; returns when done).
+  const Kind kd = kind_of(A);
+  if (kd == K_NONE || kind_of(C) != kd || kind_of(B) != kd || kind_of(info) != kd)
+    return status(res, PB_INFO_UNSUPPORTED, "A, C, B and info must be all device or all host pointers");
+  const Kind kn = kind_of(n);
+  if (kn == K_NONE || kind_of(offset) != kn || (kd == K_HOST && kn != K_HOST))
+    return status(res, PB_INFO_UNSUPPORTED, "n and offset must share one memory kind (host with host matrices)");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (kd == K_HOST) cudaStreamSynchronize(s);  // earlier work on the caller's stream (ADVICE: host calls)
+  mempool_keep();
   ChainLaunch L;
   L.pm = pm;
-  L.n = n; L.offset = offset;
-  L.A = A; L.C = C; L.B = B;
-  L.info = info;
   L.batch = batch; L.max_n = max_n;
-  cudaError_t e = chain_launch(L, (cudaStream_t)stream);
+  std::vector<void*> scratch;
+  auto dalloc = [&](size_t bytes) -> void* {
+    void* q = nullptr;
+    if (cudaMallocAsync(&q, std::max<size_t>(bytes, 16), s) != cudaSuccess) return nullptr;
+    scratch.push_back(q);
+    return q;
+  };
+  cudaError_t e = cudaSuccess;
+  long long extent = 0;  // doubles spanned by the matrices (host matrices only)
+  if (kn == K_HOST) {
+    for (int p = 0; p < batch; ++p) {
+      if (n[p] < 0 || n[p] > max_n) return fail(res, routine, 2, 2, "n[p] is negative or above max_n");
+      if (offset[p] < 0) return fail(res, routine, 3, 3, "offset[p] is negative");
+      extent = std::max(extent, offset[p] + (long long)n[p] * n[p]);
+    }
+    int* dn = (int*)dalloc(sizeof(int) * batch);
+    long long* doff = (long long*)dalloc(sizeof(long long) * batch);
+    if (!dn || !doff) e = cudaErrorMemoryAllocation;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dn, n, sizeof(int) * batch, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(doff, offset, sizeof(long long) * batch, cudaMemcpyHostToDevice, s);
+    L.n = dn; L.offset = doff;
+    L.n_host = n; L.offset_host = offset;
+  } else {
+    L.n = n; L.offset = offset;
+  }
+  double *dA = A, *dC = C, *dB = B;
+  int* dinfo = info;
+  if (e == cudaSuccess && kd == K_HOST) {
+    const size_t bytes = sizeof(double) * (size_t)extent;
+    dA = (double*)dalloc(bytes); dC = (double*)dalloc(bytes); dB = (double*)dalloc(bytes);
+    dinfo = (int*)dalloc(sizeof(int) * batch);
+    if (!dA || !dC || !dB || !dinfo) e = cudaErrorMemoryAllocation;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dA, A, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dC, C, bytes, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dB, B, bytes, cudaMemcpyHostToDevice, s);
+  }
+  L.A = dA; L.C = dC; L.B = dB;
+  L.info = dinfo;
+  if (e == cudaSuccess) e = chain_launch(L, s);
   if (e == cudaSuccess && mutation_epsilon() != 0.0)
-    e = mutate_launch(B, 0, offset, batch, mutation_epsilon(), (cudaStream_t)stream);
+    e = mutate_launch(dB, 0, L.offset, batch, mutation_epsilon(), s);
+  if (e == cudaSuccess && kd == K_HOST) {
+    const size_t bytes = sizeof(double) * (size_t)extent;
+    e = cudaMemcpyAsync(C, dC, bytes, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(B, dB, bytes, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int) * batch, cudaMemcpyDeviceToHost, s);
+  }
+  for (void* q : scratch) cudaFreeAsync(q, s);
+  if (e == cudaSuccess && kd == K_HOST) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return cuda_fail(res, routine, e);
   return finish(res, 0, 0);
 }

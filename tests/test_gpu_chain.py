@@ -152,3 +152,38 @@ def test_chain_cfg5_full_batch_properties(pb, cuda):
         e2 = (torch.linalg.matrix_norm(x @ l.transpose(1, 2) - b) / torch.linalg.matrix_norm(b)).max().item()
         worst = max(worst, e1 / tol(n), e2 / tol(n))
     assert worst <= 1.0, worst
+
+
+@pytest.mark.parametrize("layout", ["C", "P"])
+def test_chain_host_plan_and_host_pointers(pb, cuda, layout):
+    """pb_chain_vbatched with host n / offset (device matrices: no synchronisation) and with
+    everything on the host (staged): bit-identical to the all-device call."""
+    import torch
+    rng = np.random.default_rng(21)
+    batch = 40
+    ns = (rng.integers(1, 65, batch) * 4).astype(np.int32)
+    ns[:3] = [4, 168, 256]
+    offs = np.concatenate([[0], np.cumsum(ns.astype(np.int64) ** 2)[:-1]]).astype(np.int64)
+    total = int((ns.astype(np.int64) ** 2).sum())
+    A = rng.uniform(-1, 1, total); B = rng.uniform(-1, 1, total); C = np.zeros(total)
+    for p, n in enumerate(ns):
+        blk = np.zeros((n, n)); blk[np.arange(n), np.arange(n)] = n
+        C[offs[p]:offs[p] + n * n] = blk.reshape(-1, order="F") if layout == "C" else pack(blk)
+    runs = []
+    for mode in ("device", "host_plan", "host"):
+        if mode == "host":
+            a, c, b = A.copy(), C.copy(), B.copy()
+            info = np.full(batch, -9, np.int32)
+            assert pb.chain_vbatched(layout, ns, offs, a, c, b, info, batch, 256).ok()
+            runs.append((c, b, info))
+            continue
+        a, c, b = (torch.from_numpy(x.copy()).to(cuda) for x in (A, C, B))
+        info = torch.full((batch,), -9, dtype=torch.int32, device=cuda)
+        n_arg = torch.from_numpy(ns).to(cuda) if mode == "device" else ns
+        o_arg = torch.from_numpy(offs).to(cuda) if mode == "device" else offs
+        assert pb.chain_vbatched(layout, n_arg, o_arg, a, c, b, info, batch, 256).ok()
+        torch.cuda.synchronize()
+        runs.append((c.cpu().numpy(), b.cpu().numpy(), info.cpu().numpy()))
+    for other in runs[1:]:
+        assert (other[2] == 0).all()
+        assert same_bits(other[0], runs[0][0]) and same_bits(other[1], runs[0][1])
