@@ -5,7 +5,7 @@
 //   syrk_potrf_nd (level3.hpp:533-575): n <= 160 runs in ONE kernel — the
 //   pipelined CTA Cholesky with the prologue S = C + A B^T on the tensor cores
 //   and the LowerZero band store; larger n: gemm engine (lower S in D) ->
-//   unpack -> blocked column-major potrf -> pack with the band zeros.
+//   blocked panel-major potrf in place (band zeros by its diagonal blocks).
 //
 //   chain (pb_chain_vbatched): problems are split on the host by order.
 //   n <= 160: variable-batch kernels straight on the caller's buffers
@@ -26,35 +26,6 @@
 namespace pbg {
 
 // ------------------------------------------------------------------ layout kernels
-// dst (cm, ld = n) <- src (pm, cn = round_up(n, 4)), per problem (same offsets
-// or strides for both); only the lower triangle when `lower`.
-__global__ void pm_to_cm_kernel(const double* src, long long ss, double* dst, long long sd, int n, int cn,
-                                int lower) {
-  const long long p = blockIdx.y;
-  const double* s = src + p * ss;
-  double* d = dst + p * sd;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
-    const int j = e / n, i = e - j * n;
-    if (lower && i < j) continue;
-    d[i + (long long)j * n] = s[(long long)(i >> 2) * 4 * cn + (long long)j * 4 + (i & 3)];
-  }
-}
-// dst (pm) <- src (cm lower, ld = n) with the LowerZero band zeros
-// (strictly-upper entries of each 8-row diagonal band written as 0).
-__global__ void cm_to_pm_band_kernel(const double* src, long long ss, double* dst, long long sd, int n,
-                                     int cn) {
-  const long long p = blockIdx.y;
-  const double* s = src + p * ss;
-  double* d = dst + p * sd;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
-    const int j = e / n, i = e - j * n;
-    double v;
-    if (i >= j) v = s[i + (long long)j * n];
-    else if ((i >> 3) == (j >> 3)) v = 0.0;
-    else continue;
-    d[(long long)(i >> 2) * 4 * cn + (long long)j * 4 + (i & 3)] = v;
-  }
-}
 // Square n x n blocks: ws[q] <-> base + offs[idx[q]] (ld preserved).
 __global__ void gather_kernel(const double* base, const long long* offs, const int* idx, double* ws, int nn) {
   const int q = blockIdx.y;
@@ -104,20 +75,11 @@ cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
   if (L.k > 0) e = gemm_launch(g, s);
   else e = scale_launch(1, g.o, L.n, L.n, 1.0, 1, L.batch, s);
   if (e != cudaSuccess) return e;
-  double* ws = nullptr;
-  const long long nn = (long long)L.n * L.n;
-  e = cudaMallocAsync(&ws, sizeof(double) * nn * L.batch, s);
-  if (e != cudaSuccess) return e;
-  pm_to_cm_kernel<<<grid2(nn, L.batch), 256, 0, s>>>(L.d, L.sd, ws, nn, L.n, L.cnd, 1);
+  // factor D in place, panel-major, with the LowerZero band zeros
   PotrfLaunch P;
-  P.a = ws; P.stride = nn; P.lda = L.n; P.n = L.n; P.upper = 0; P.info = L.info; P.batch = L.batch;
-  e = potrf_launch(P, s);
-  if (e == cudaSuccess) {
-    cm_to_pm_band_kernel<<<grid2(nn, L.batch), 256, 0, s>>>(ws, nn, L.d, L.sd, L.n, L.cnd);
-    e = cudaGetLastError();
-  }
-  cudaFreeAsync(ws, s);
-  return e;
+  P.a = L.d; P.stride = L.sd; P.lda = L.cnd; P.n = L.n; P.pm = 1; P.zero_fill = 1;
+  P.info = L.info; P.batch = L.batch;
+  return potrf_launch(P, s);
 }
 
 // ------------------------------------------------------------------ chain (cfg 5)

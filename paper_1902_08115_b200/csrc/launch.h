@@ -75,7 +75,8 @@ namespace pbg {
 struct PotrfLaunch {
   double* a = nullptr;
   long long stride = 0;
-  int lda = 0, n = 0, upper = 0;
+  int lda = 0, n = 0, upper = 0;  // lda: leading dimension (cm) or panel width cn (pm)
+  int pm = 0, zero_fill = 0;      // panel-major (lower only); LowerZero band zeros (syrk_potrf_nd)
   int* info = nullptr;
   int batch = 0;
 };

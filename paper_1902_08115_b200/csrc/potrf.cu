@@ -6,7 +6,9 @@
 //             pipelined left-looking panels on DMMA);
 //   n > 160   right-looking blocked over 128-column panels, composed here from
 //             potrf_cta (diagonal block) -> trsm_rlt (panel solve) -> the DMMA
-//             gemm engine (lower syrk of the trailing matrix).
+//             gemm engine (lower syrk of the trailing matrix); column-major
+//             (lower / upper) or panel-major (lower, with the LowerZero band
+//             zeros of syrk_potrf_nd) in place.
 #include <algorithm>
 #include <cstdlib>
 
@@ -24,7 +26,16 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     return e ? atoi(e) : kPotrfSmemMax + 1;
   }();
   if (L.n <= kPotrfSmemMax && L.n < blocked_from)
-    return potrf_cta_launch(L.a, L.stride, nullptr, nullptr, L.lda, L.n, L.upper, 0, 0, L.info, 0, 0, L.batch, s);
+    return potrf_cta_launch(L.a, L.stride, nullptr, nullptr, L.lda, L.n, L.upper, L.pm, L.zero_fill, L.info, 0, 0,
+                            L.batch, s);
+  if (L.pm && L.upper) return cudaErrorInvalidValue;
+  // element (i, j) of the lower problem: i + j*lda (lower), j + i*lda (upper),
+  // (i/4)*4*cn + 4j + i%4 (panel-major; block corners are multiples of 8, so
+  // every sub-block is again a panel-major view with the same cn)
+  auto at = [&](int i, int j) -> long long {
+    if (L.pm) return (long long)(i >> 2) * 4 * L.lda + (long long)j * 4 + (i & 3);
+    return L.upper ? (long long)j + (long long)i * L.lda : (long long)i + (long long)j * L.lda;
+  };
   // Right-looking blocked over 128-column panels: potrf(A11) -> A21 = A21 L11^{-T}
   // (trsm) -> A22 -= A21 A21^T (DMMA syrk) -> recurse on A22.  Problems whose
   // info turned nonzero are skipped by every later stage.
@@ -36,12 +47,13 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
   for (int c0 = 0; c0 < L.n; c0 += nb) {
     const int w = std::min(nb, L.n - c0), rest = L.n - c0 - w;
     // element (i, j) of the lower problem lives at i + j*lda (lower) or j + i*lda (upper)
-    double* a11 = L.a + (long long)c0 + (long long)c0 * L.lda;
-    cudaError_t e = potrf_cta_launch(a11, L.stride, nullptr, nullptr, L.lda, w, L.upper, 0, 0, L.info, c0, c0 > 0, L.batch, s);
+    double* a11 = L.a + at(c0, c0);
+    cudaError_t e = potrf_cta_launch(a11, L.stride, nullptr, nullptr, L.lda, w, L.upper, L.pm, L.zero_fill, L.info,
+                                     c0, c0 > 0, L.batch, s);
     if (e != cudaSuccess) return e;
     if (!rest) break;
     TrsmLaunch T;
-    T.pm = 0;
+    T.pm = L.pm;
     T.twin = L.upper;      // upper: rows of the effective problem are columns
     T.lower = 1;
     T.trans = 1;           // X * L11^T = A21
@@ -51,8 +63,7 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     T.alpha = 1.0;
     T.a = a11; T.sa = L.stride; T.lda = L.lda;
     // Lower: A21 rows c0+w.. at (c0+w) + c0*lda.  Upper: twin view of A12 at c0 + (c0+w)*lda.
-    double* b = L.upper ? L.a + (long long)c0 + (long long)(c0 + w) * L.lda
-                        : L.a + (long long)(c0 + w) + (long long)c0 * L.lda;
+    double* b = L.upper ? L.a + (long long)c0 + (long long)(c0 + w) * L.lda : L.a + at(c0 + w, c0);
     T.b = b; T.sb = L.stride; T.ldb = L.lda;
     T.d = b; T.sd = L.stride; T.ldd = L.lda;
     T.info = L.info;
@@ -62,8 +73,11 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     e = trsm_launch(T, s);
     if (e != cudaSuccess) return e;
     GemmLaunch g;
-    double* a22 = L.a + (long long)(c0 + w) + (long long)(c0 + w) * L.lda;
-    if (!L.upper) {  // A22 -= A21 A21^T  (syrk 'l','n')
+    double* a22 = L.a + at(c0 + w, c0 + w);
+    if (L.pm) {      // A22 -= A21 A21^T, panel-major in and out
+      g.lay_a = g.lay_b = L_PMX;
+      g.out_pm = 1;
+    } else if (!L.upper) {  // A22 -= A21 A21^T  (syrk 'l','n')
       g.lay_a = g.lay_b = L_MNC;
     } else {         // A22(upper) -= A12^T A12 (syrk 'u','t')
       g.lay_a = g.lay_b = L_KC;
