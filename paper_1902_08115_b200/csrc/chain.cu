@@ -1,6 +1,6 @@
 // Fused panel-major syrk+potrf (syrk_potrf_nd) and the variable-size
 // Riccati-like chain of config 5 (dsyrk -> dpotrf -> dtrsm), plus the batched
-// layout kernels they need (column-major <-> panel-major, gathers).
+// small kernels they need (the per-class info scatter).
 //
 //   syrk_potrf_nd (level3.hpp:533-575): n <= 160 runs in ONE kernel — the
 //   pipelined CTA Cholesky with the prologue S = C + A B^T on the tensor cores
@@ -9,10 +9,10 @@
 //
 //   chain (pb_chain_vbatched): problems are split on the host by order.
 //   n <= 160: variable-batch kernels straight on the caller's buffers
-//     column-major: syrk (lower C += A A^T) -> potrf -> trsm X L^T = B
+//     column-major: fused syrk+potrf (n > 32; syrk -> potrf_reg below) -> trsm X L^T = B
 //     panel-major : fused syrk+potrf (prologue)  -> trsm_rltn
-//   n > 160: problems of equal order are gathered into a strided workspace,
-//   run through the strided batched kernels, and scattered back.
+//   n > 160: per distinct order, the strided kernels (engine syrk, blocked
+//   potrf, trsm_rlt) run on the caller's buffers through per-problem offsets.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,32 +25,38 @@
 
 namespace pbg {
 
-// ------------------------------------------------------------------ layout kernels
-// Square n x n blocks: ws[q] <-> base + offs[idx[q]] (ld preserved).
-__global__ void gather_kernel(const double* base, const long long* offs, const int* idx, double* ws, int nn) {
+// ------------------------------------------------------------------ small kernels
+// Square n x n problems: ws[q] <- base + offs[q] (all of it) / base + offs[q] <- ws[q] (lower triangle)
+__global__ void gather_kernel(const double* base, const long long* offs, double* ws, int n) {
   const int q = blockIdx.y;
-  const double* s = base + offs[idx[q]];
+  const long long nn = (long long)n * n;
+  const double* s = base + offs[q];
   double* d = ws + (long long)q * nn;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += gridDim.x * blockDim.x) d[e] = s[e];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x)
+    d[e] = s[e];
 }
-__global__ void scatter_kernel(const double* ws, double* base, const long long* offs, const int* idx, int nn) {
+__global__ void scatter_lower_kernel(const double* ws, double* base, const long long* offs, int n) {
   const int q = blockIdx.y;
+  const long long nn = (long long)n * n;
   const double* s = ws + (long long)q * nn;
-  double* d = base + offs[idx[q]];
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += gridDim.x * blockDim.x) d[e] = s[e];
+  double* d = base + offs[q];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / n), i = (int)(e - (long long)j * n);
+    if (i >= j) d[e] = s[e];
+  }
+}
+static dim3 grid2(long long work, int batch) {
+  return dim3((unsigned)std::max<long long>(1, std::min<long long>((work + 255) / 256, 64)), (unsigned)batch);
 }
 __global__ void scatter_info_kernel(const int* src, const int* idx, int* info, int count) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < count; q += gridDim.x * blockDim.x) info[idx[q]] = src[q];
 }
 
-static dim3 grid2(long long work, int batch) {
-  return dim3((unsigned)std::max<long long>(1, std::min<long long>((work + 255) / 256, 64)), (unsigned)batch);
-}
 
 // ------------------------------------------------------------------ syrk_potrf_nd
 cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.n <= 0) return cudaSuccess;
-  const bool fused_ok = L.n <= 160 && (L.k == 0 || (L.cna == L.cnb && L.sa == L.sb));
+  const bool fused_ok = L.n <= 160 && !L.offs && (L.k == 0 || (L.cna == L.cnb && L.sa == L.sb));
   if (fused_ok)
     return syrk_potrf_cta_launch(L.d, L.sd, nullptr, nullptr, L.cnd, L.c, L.sc, L.cnc, L.k ? L.a : nullptr,
                                  L.k ? L.b : nullptr, L.sa, L.k, L.cna, L.n, 1, 1, L.info, L.batch, s);
@@ -61,11 +67,12 @@ cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
   g.lay_a = L_PMX;
   g.lay_b = L_PMX;
   g.a.base = L.a; g.a.stride = L.sa; g.a.ld = L.cna;
-  g.a.bulk = ((reinterpret_cast<uintptr_t>(L.a) & 15) == 0) && L.sa % 2 == 0;
+  g.a.bulk = ((reinterpret_cast<uintptr_t>(L.a) & 15) == 0) && (L.offs ? L.offs_even != 0 : L.sa % 2 == 0);
   g.b.base = L.b; g.b.stride = L.sb; g.b.ld = L.cnb;
-  g.b.bulk = ((reinterpret_cast<uintptr_t>(L.b) & 15) == 0) && L.sb % 2 == 0;
+  g.b.bulk = ((reinterpret_cast<uintptr_t>(L.b) & 15) == 0) && (L.offs ? L.offs_even != 0 : L.sb % 2 == 0);
   g.o.c = L.c; g.o.d = L.d; g.o.sc = L.sc; g.o.sd = L.sd; g.o.ldc = L.cnc; g.o.ldd = L.cnd;
   g.o.vec = 0;
+  g.a.offs = g.b.offs = g.o.offs = L.offs;
   g.m = g.n = L.n;
   g.k = L.k;
   g.alpha = 1.0;
@@ -78,6 +85,7 @@ cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
   // factor D in place, panel-major, with the LowerZero band zeros
   PotrfLaunch P;
   P.a = L.d; P.stride = L.sd; P.lda = L.cnd; P.n = L.n; P.pm = 1; P.zero_fill = 1;
+  P.offs = L.offs; P.offs_even = L.offs_even;
   P.info = L.info; P.batch = L.batch;
   return potrf_launch(P, s);
 }
@@ -186,31 +194,41 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
     cudaFreeAsync(d_off, s);
     if (e != cudaSuccess) return e;
   }
-  // large orders: gather -> strided batched chain -> scatter, per distinct n
+  // large orders, per distinct n: the syrk, the blocked Cholesky and the solve
+  // run straight on the caller's buffers through per-problem offsets (the
+  // class's members), so nothing is gathered or scattered
   for (auto& kv : big) {
     const int n = kv.first, cnt = (int)kv.second.size();
-    const long long nn = (long long)n * n;  // n % 4 == 0 in panel-major: pm = cn = n
-    double *wa = nullptr, *wc = nullptr;
     int *d_i = nullptr, *w_info = nullptr;
-    long long* d_ob = nullptr;  // B stays in place: the solve reads and writes it at its own offsets
-    if ((e = cudaMallocAsync(&wa, sizeof(double) * nn * cnt * 2, s)) != cudaSuccess ||
-        (e = cudaMallocAsync(&d_i, sizeof(int) * cnt, s)) != cudaSuccess ||
+    long long* d_o = nullptr;
+    if ((e = cudaMallocAsync(&d_i, sizeof(int) * cnt, s)) != cudaSuccess ||
         (e = cudaMallocAsync(&w_info, sizeof(int) * cnt, s)) != cudaSuccess ||
-        (e = cudaMallocAsync(&d_ob, sizeof(long long) * cnt, s)) != cudaSuccess)
+        (e = cudaMallocAsync(&d_o, sizeof(long long) * cnt, s)) != cudaSuccess)
       return e;
-    wc = wa + nn * cnt;
     std::vector<long long> ob(cnt);
-    for (int q = 0; q < cnt; ++q) ob[q] = ov[kv.second[q]];
+    bool even = true;
+    for (int q = 0; q < cnt; ++q) {
+      ob[q] = ov[kv.second[q]];
+      even = even && (ob[q] % 2 == 0);
+    }
     cudaMemcpyAsync(d_i, kv.second.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(d_ob, ob.data(), sizeof(long long) * cnt, cudaMemcpyHostToDevice, s);
-    dim3 gg = grid2(nn, cnt);
-    gather_kernel<<<gg, 256, 0, s>>>(L.A, L.offset, d_i, wa, (int)nn);
-    gather_kernel<<<gg, 256, 0, s>>>(L.C, L.offset, d_i, wc, (int)nn);
+    cudaMemcpyAsync(d_o, ob.data(), sizeof(long long) * cnt, cudaMemcpyHostToDevice, s);
+    double* wc = nullptr;  // column-major: the factor's workspace (S = C + A A^T, then L)
+    double* wa = nullptr;
     if (!L.pm) {
-      GemmLaunch g;  // dsyrk('l','n'): C += A A^T
+      // column-major: the engine's tensor-map path needs strided operands (its
+      // per-column bulk copies measured 1.7x slower here), so A is gathered once,
+      // S = C + A A^T lands in a strided workspace (C read through the offsets),
+      // is factored there, and only L's lower triangle goes back to C
+      const long long nn = (long long)n * n;
+      if ((e = cudaMallocAsync(&wa, sizeof(double) * nn * cnt * 2, s)) != cudaSuccess) return e;
+      wc = wa + nn * cnt;
+      gather_kernel<<<grid2(nn, cnt), 256, 0, s>>>(L.A, d_o, wa, n);
+      GemmLaunch g;  // dsyrk('l','n'): S = C + A A^T
       g.lay_a = g.lay_b = L_MNC;
       g.a.base = g.b.base = wa; g.a.stride = g.b.stride = nn; g.a.ld = g.b.ld = n; g.a.bulk = g.b.bulk = 1;
-      g.o.c = wc; g.o.d = wc; g.o.sc = g.o.sd = nn; g.o.ldc = g.o.ldd = n; g.o.vec = 1;
+      g.o.c = L.C; g.o.offs_c = d_o; g.o.d = wc; g.o.sd = nn; g.o.ldc = g.o.ldd = n;
+      g.o.vec = even && n % 2 == 0 && (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
       g.m = g.n = g.k = n;
       g.alpha = 1.0; g.beta = 1.0; g.uplo = 1; g.batch = cnt;
       e = gemm_launch(g, s);
@@ -221,8 +239,10 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       }
     } else {
       SyrkPotrfLaunch S;
-      S.a = S.b = wa; S.c = wc; S.d = wc;
-      S.sa = S.sb = S.sc = S.sd = nn;
+      S.a = S.b = L.A; S.c = L.C; S.d = L.C;
+      S.offs = d_o;
+      S.offs_even = even && (reinterpret_cast<uintptr_t>(L.A) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
       S.cna = S.cnb = S.cnc = S.cnd = n;
       S.n = S.k = n;
       S.info = w_info;
@@ -235,23 +255,26 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       T.lower = 1; T.trans = 1; T.unit = 0;
       T.mm = T.nn = n;
       T.alpha = 1.0;
-      T.a = wc; T.sa = nn; T.lda = n;
+      T.a = L.pm ? L.C : wc; T.offs_a = L.pm ? d_o : nullptr; T.sa = (long long)n * n; T.lda = n;
       T.b = L.B; T.ldb = n;
       T.d = L.B; T.ldd = n;
-      T.offs_b = d_ob;
+      T.offs_b = d_o;
       T.info = w_info;
       T.skip_nonzero = 1;
       T.batch = cnt;
       e = trsm_launch(T, s);
     }
+    if (e == cudaSuccess && !L.pm) {
+      scatter_lower_kernel<<<grid2((long long)n * n, cnt), 256, 0, s>>>(wc, L.C, d_o, n);
+      e = cudaGetLastError();
+    }
     if (e == cudaSuccess) {
-      scatter_kernel<<<gg, 256, 0, s>>>(wc, L.C, L.offset, d_i, (int)nn);
       scatter_info_kernel<<<std::max(1, (cnt + 255) / 256), 256, 0, s>>>(w_info, d_i, L.info, cnt);
       e = cudaGetLastError();
     }
-    cudaFreeAsync(wa, s);
+    if (wa) cudaFreeAsync(wa, s);
     cudaFreeAsync(d_i, s);
-    cudaFreeAsync(d_ob, s);
+    cudaFreeAsync(d_o, s);
     cudaFreeAsync(w_info, s);
     if (e != cudaSuccess) return e;
   }

@@ -86,6 +86,7 @@ struct KParams {
   OpDesc a, b;
   OutDesc o;
   int tmaA, tmaB;
+  int bulkA, bulkB;                // per-problem offsets: column / panel bulk copies instead of a tensor map
   int batched_mapA, batched_mapB;  // tensor map has a problem dimension
   int m, n, k;
   double alpha, beta;
@@ -153,7 +154,7 @@ template <int L>
 __device__ __forceinline__ void elem_side(const OpDesc& d, int p, int x0, int xvalid, int l0,
                                           int kvalid, double* s, int lane) {
   using T = LayT<L>;
-  const double* g = d.base + (long long)p * d.stride;
+  const double* g = d.base + (d.offs ? d.offs[p] : (long long)p * d.stride);
   const int kvalid4 = (kvalid + 3) & ~3;
   for (int e = lane; e < kvalid4 * TM; e += 32) {
     int x, l;
@@ -161,6 +162,39 @@ __device__ __forceinline__ void elem_side(const OpDesc& d, int p, int x0, int xv
     bool v = x < xvalid && l < kvalid;
     const double* src = v ? g + T::g(d.ld, x0 + x, l0 + l) : d.base;
     cp_async8(s + T::at(x, l), src, v);
+  }
+}
+
+// Producer, per-problem-offset path (no tensor map can describe the batch):
+// one bulk copy per column (column-major, x contiguous: xvalid doubles) or per
+// 4-row panel (panel-major: 4 kvalid doubles), spread over the lanes; k
+// columns in [kvalid, kvalid rounded up to 4) are zeroed.  Lane 0 registers
+// the chunk's bytes on the stage barrier once, before any lane issues.
+template <int L>
+__device__ __forceinline__ void bulk_side(const OpDesc& d, int p, int x0, int xvalid, int l0, int kvalid, double* s,
+                                          int lane, uint64_t* bar) {
+  const double* g = d.base + (d.offs ? d.offs[p] : (long long)p * d.stride);
+  const int kvalid4 = (kvalid + 3) & ~3;
+  if constexpr (L == L_MNC) {
+    const uint32_t bytes = 8u * (uint32_t)xvalid;  // xvalid even (host check)
+    if (lane == 0) mbar_expect_tx(bar, bytes * (uint32_t)kvalid);
+    __syncwarp();
+    const int l = lane;  // BK == 32 columns, one per lane
+    if (l < kvalid) {
+      bulk_g2s(s + LayT<L>::at(0, l), g + LayT<L>::g(d.ld, x0, l0 + l), bytes, bar);
+    } else if (l < kvalid4) {
+      for (int x = 0; x < TM; x += 2) sts128(smem_u32(s + LayT<L>::at(x, l)), 0.0, 0.0);
+    }
+  } else {  // L_PMX: panel q = rows x0 + 4q .. x0 + 4q + 3, columns l0 .. l0 + kvalid - 1 contiguous
+    const uint32_t bytes = 32u * (uint32_t)kvalid;
+    const int np = min(TM / 4, (xvalid + 3) >> 2);
+    if (lane == 0) mbar_expect_tx(bar, bytes * (uint32_t)np);
+    __syncwarp();
+    const int q = lane;
+    if (q < np) {
+      bulk_g2s(s + LayT<L>::at(4 * q, 0), g + LayT<L>::g(d.ld, x0 + 4 * q, l0), bytes, bar);
+      for (int e = 4 * kvalid; e < 4 * kvalid4; e += 2) sts128(smem_u32(s + LayT<L>::at(4 * q, 0) + e), 0.0, 0.0);
+    }
   }
 }
 
@@ -215,12 +249,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
           if (P.tmaA) tma_side<LA>(&P.tmA, P.batched_mapA, p, i0, l0, sA, &full[stage]);
           if (P.tmaB) tma_side<LB>(&P.tmB, P.batched_mapB, p, j0, l0, sB, &full[stage]);
         }
-        if (!P.tmaA || !P.tmaB) {
+        if constexpr (LA == L_MNC || LA == L_PMX)
+          if (P.bulkA) bulk_side<LA>(P.a, p, i0, mvalid, l0, kvalid, sA, lane, &full[stage]);
+        if constexpr (LB == L_MNC || LB == L_PMX)
+          if (P.bulkB) bulk_side<LB>(P.b, p, j0, nvalid, l0, kvalid, sB, lane, &full[stage]);
+        const bool elemA = !P.tmaA && !P.bulkA, elemB = !P.tmaB && !P.bulkB;
+        if (elemA || elemB) {
           fence_proxy_async();
-          if (!P.tmaA) elem_side<LA>(P.a, p, i0, mvalid, l0, kvalid, sA, lane);
-          if (!P.tmaB) elem_side<LB>(P.b, p, j0, nvalid, l0, kvalid, sB, lane);
+          if (elemA) elem_side<LA>(P.a, p, i0, mvalid, l0, kvalid, sA, lane);
+          if (elemB) elem_side<LB>(P.b, p, j0, nvalid, l0, kvalid, sB, lane);
+          mbar_arrive_cpasync(&full[stage]);
+        } else {
+          mbar_arrive(&full[stage]);  // (release: covers the zero-fill stores of bulk sides)
         }
-        mbar_arrive_cpasync(&full[stage]);
         if (++stage == P.nstages) { stage = 0; phase ^= 1; }
       }
     }
@@ -238,7 +279,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
   auto load_c = [&](long long it, double (&dst)[4][2][2]) {
     int p, tm, tn;
     decode_item(P, it, p, tm, tn);
-    const double* cbase = P.o.c + (long long)p * P.o.sc;
+    const double* cbase =
+        P.o.c + (P.o.offs_c ? P.o.offs_c[p] : P.o.offs ? P.o.offs[p] : (long long)p * P.o.sc);
     const bool live = !(P.skip && P.skip[p]);
 #pragma unroll
     for (int f = 0; f < 4; ++f)
@@ -274,7 +316,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
     }
     if (P.skip && P.skip[p]) continue;
     const int i0 = tm * TM, j0 = tn * TN;
-    double* dbase = P.o.d + (long long)p * P.o.sd;
+    double* dbase = P.o.d + (P.o.offs ? P.o.offs[p] : (long long)p * P.o.sd);
 
     double acc[4][2][2];
 #pragma unroll
@@ -358,8 +400,10 @@ __global__ void scale_kernel(OutDesc o, int m, int n, double beta, int uplo, lon
     if (uplo == 1 && i < j) continue;
     if (uplo == 2 && i > j) continue;
     double v = 0.0 * 0.0;  // scale_ab(alpha = 0): 0*0 (+ beta*c) — micro_kernel.hpp:263-273
-    if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, o.c[(long long)p * o.sc + out_off<OUT_PM>(o.ldc, i, j)]));
-    o.d[(long long)p * o.sd + out_off<OUT_PM>(o.ldd, i, j)] = v;
+    const long long oc = o.offs_c ? o.offs_c[p] : o.offs ? o.offs[p] : (long long)p * o.sc;
+    const long long od = o.offs ? o.offs[p] : (long long)p * o.sd;
+    if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, o.c[oc + out_off<OUT_PM>(o.ldc, i, j)]));
+    o.d[od + out_off<OUT_PM>(o.ldd, i, j)] = v;
   }
 }
 
@@ -478,8 +522,18 @@ cudaError_t gemm_launch(const GemmLaunch& g, cudaStream_t s) {
     const char* e = getenv("PBGPU_NO_TMA");
     return e && e[0] == '1';
   }();
-  if (!no_tma && g.a.bulk) P.tmaA = make_map(&P.tmA, g.lay_a, g.a, g.m, g.k, g.batch, &P.batched_mapA);
-  if (!no_tma && g.b.bulk) P.tmaB = make_map(&P.tmB, g.lay_b, g.b, g.n, g.k, g.batch, &P.batched_mapB);
+  // per-problem offsets have no tensor-map form: those sides stream by column /
+  // panel bulk copies (bulk = every problem base 16-byte aligned, caller-checked)
+  if (!no_tma && g.a.bulk && !g.a.offs) P.tmaA = make_map(&P.tmA, g.lay_a, g.a, g.m, g.k, g.batch, &P.batched_mapA);
+  if (!no_tma && g.b.bulk && !g.b.offs) P.tmaB = make_map(&P.tmB, g.lay_b, g.b, g.n, g.k, g.batch, &P.batched_mapB);
+  auto bulk_ok = [](int lay, const OpDesc& d, int x) {
+    if (!d.offs || !d.bulk) return false;
+    if (lay == L_PMX) return true;
+    return lay == L_MNC && d.ld % 2 == 0 && x % 2 == 0;
+  };
+  P.bulkA = !P.tmaA && bulk_ok(g.lay_a, g.a, g.m);
+  P.bulkB = !P.tmaB && bulk_ok(g.lay_b, g.b, g.n);
+  if ((P.bulkA && !P.tmaB && !P.bulkB) || (P.bulkB && !P.tmaA && !P.bulkA)) P.bulkA = P.bulkB = 0;
   if (!g.out_pm) {
     if (g.lay_a == L_MNC && g.lay_b == L_MNC) return launch_t<L_MNC, L_MNC, 0>(P, s);
     if (g.lay_a == L_MNC && g.lay_b == L_KC) return launch_t<L_MNC, L_KC, 0>(P, s);

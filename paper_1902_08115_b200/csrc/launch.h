@@ -22,6 +22,7 @@ struct OpDesc {
   long long stride = 0;          // elements between consecutive problems
   int ld = 0;                    // leading dimension (cm) or panel width cn (pm)
   int bulk = 0;                  // 1 when every bulk copy is 16-byte aligned
+  const long long* offs = nullptr;  // optional per-problem element offsets (replace p * stride; no TMA)
 };
 
 struct OutDesc {
@@ -30,6 +31,8 @@ struct OutDesc {
   long long sc = 0, sd = 0;
   int ldc = 0, ldd = 0;  // ld (cm) or cn (pm)
   int vec = 0;           // 1 when 16-byte paired accesses are aligned
+  const long long* offs = nullptr;    // optional per-problem element offsets of d (and c, unless offs_c)
+  const long long* offs_c = nullptr;  // optional per-problem element offsets of c alone
 };
 
 struct GemmLaunch {
@@ -77,6 +80,8 @@ struct PotrfLaunch {
   long long stride = 0;
   int lda = 0, n = 0, upper = 0;  // lda: leading dimension (cm) or panel width cn (pm)
   int pm = 0, zero_fill = 0;      // panel-major (lower only); LowerZero band zeros (syrk_potrf_nd)
+  const long long* offs = nullptr;  // optional per-problem element offsets (replace p * stride)
+  int offs_even = 0;                // caller's promise: every offset is even (16-byte bulk copies)
   int* info = nullptr;
   int batch = 0;
 };
@@ -156,8 +161,9 @@ struct TrsmLaunch {
   // round_up(n, 4)) and element offsets shared by a, b and d
   const int* nvec = nullptr;
   const long long* offs = nullptr;
-  // optional: uniform strided a (sa) with b / d at per-problem element offsets
-  // (the chain's large orders: the factor in a gathered workspace, B in place)
+  // optional per-problem element offsets of a (offs_a) and of b / d (offs_b)
+  // with a uniform order (the chain's large orders and the blocked potrf over them)
+  const long long* offs_a = nullptr;
   const long long* offs_b = nullptr;
 };
 cudaError_t trsm_launch(const TrsmLaunch& L, cudaStream_t s);
@@ -180,6 +186,8 @@ struct SyrkPotrfLaunch {
   const double *a = nullptr, *b = nullptr, *c = nullptr;
   double* d = nullptr;
   long long sa = 0, sb = 0, sc = 0, sd = 0;
+  const long long* offs = nullptr;  // optional per-problem offsets of a, b, c and d (replace the strides)
+  int offs_even = 0;                // caller's promise: every offset is even
   int cna = 0, cnb = 0, cnc = 0, cnd = 0;
   int n = 0, k = 0;
   int* info = nullptr;

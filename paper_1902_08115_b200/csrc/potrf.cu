@@ -26,7 +26,7 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     return e ? atoi(e) : kPotrfSmemMax + 1;
   }();
   if (L.n <= kPotrfSmemMax && L.n < blocked_from)
-    return potrf_cta_launch(L.a, L.stride, nullptr, nullptr, L.lda, L.n, L.upper, L.pm, L.zero_fill, L.info, 0, 0,
+    return potrf_cta_launch(L.a, L.stride, L.offs, nullptr, L.lda, L.n, L.upper, L.pm, L.zero_fill, L.info, 0, 0,
                             L.batch, s);
   if (L.pm && L.upper) return cudaErrorInvalidValue;
   // element (i, j) of the lower problem: i + j*lda (lower), j + i*lda (upper),
@@ -48,7 +48,7 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     const int w = std::min(nb, L.n - c0), rest = L.n - c0 - w;
     // element (i, j) of the lower problem lives at i + j*lda (lower) or j + i*lda (upper)
     double* a11 = L.a + at(c0, c0);
-    cudaError_t e = potrf_cta_launch(a11, L.stride, nullptr, nullptr, L.lda, w, L.upper, L.pm, L.zero_fill, L.info,
+    cudaError_t e = potrf_cta_launch(a11, L.stride, L.offs, nullptr, L.lda, w, L.upper, L.pm, L.zero_fill, L.info,
                                      c0, c0 > 0, L.batch, s);
     if (e != cudaSuccess) return e;
     if (!rest) break;
@@ -62,6 +62,7 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     T.nn = w;
     T.alpha = 1.0;
     T.a = a11; T.sa = L.stride; T.lda = L.lda;
+    T.offs_a = T.offs_b = L.offs;  // (null: strided)
     // Lower: A21 rows c0+w.. at (c0+w) + c0*lda.  Upper: twin view of A12 at c0 + (c0+w)*lda.
     double* b = L.upper ? L.a + (long long)c0 + (long long)(c0 + w) * L.lda : L.a + at(c0 + w, c0);
     T.b = b; T.sb = L.stride; T.ldb = L.lda;
@@ -85,7 +86,10 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     g.a.base = g.b.base = b;
     g.a.stride = g.b.stride = L.stride;
     g.a.ld = g.b.ld = L.lda;
-    g.a.bulk = g.b.bulk = ((reinterpret_cast<uintptr_t>(b) & 15) == 0) && L.lda % 2 == 0 && L.stride % 2 == 0;
+    g.a.bulk = g.b.bulk = ((reinterpret_cast<uintptr_t>(b) & 15) == 0) && L.lda % 2 == 0 &&
+                          (L.offs ? L.offs_even != 0 : L.stride % 2 == 0);
+    g.a.offs = g.b.offs = L.offs;
+    g.o.offs = L.offs;
     g.o.c = a22;
     g.o.d = a22;
     g.o.sc = g.o.sd = L.stride;

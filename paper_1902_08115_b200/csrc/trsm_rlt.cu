@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) diag_inv8_kernel(const __grid_constant__ 
     lda = PM ? ((n + 3) & ~3) : n;
     A = L.a + L.offs[p];
   } else {
-    A = L.a + p * L.sa;
+    A = L.a + (L.offs_a ? L.offs_a[p] : p * L.sa);
   }
   if (8 * J >= n) return;
   auto el = [&](int i, int l) -> double {  // L_JJ(i, l), l <= i
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     B = L.b + L.offs[p];
     D = L.d + L.offs[p];
   } else {
-    A = L.a + p * L.sa;
+    A = L.a + (L.offs_a ? L.offs_a[p] : p * L.sa);
     B = L.b + (L.offs_b ? L.offs_b[p] : p * L.sb);
     D = L.d + (L.offs_b ? L.offs_b[p] : p * L.sd);
   }
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
 
 
 bool trsm_rlt_ok(const TrsmLaunch& L) { return !(L.twin && L.pm) && L.lower && L.trans && L.nn <= 512; }
-// (offs_b is honoured only here: trsm_launch forwards every such launch to this kernel)
+// (offs_a / offs_b are honoured only here: trsm_launch forwards every such launch to this kernel)
 
 cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.mm <= 0 || L.nn <= 0) return cudaSuccess;
