@@ -166,15 +166,18 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
   const int abs = R.ntmax * 64;
   const double alpha = L.alpha;
   // stage rows 8J..8J+7, columns 0..8J+7 of A (16-byte pairs of rows; rows past n are zero)
+  // stage rows 8J..8J+7, columns 0..8J+7 of A (16-byte pairs of rows; rows past n are zero):
+  // thread tid always copies the pair (8J + 2(tid & 3), +1) of columns tid/4, tid/4 + 32, ...
+  const bool pair_al = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (PM || lda % 2 == 0);
   auto stage = [&](int J) {
     double* ab = ab_base + (J & 1) * abs;
-    const int cols = 8 * J + 8, tot = cols * 4;
-    for (int e = tid; e < tot; e += 32 * kRltWarps) {
-      const int c = e >> 2, g2 = (e & 3) * 2, row = 8 * J + g2;
+    const int cols = 8 * J + 8, g2 = (tid & 3) * 2, row = 8 * J + g2;
+    const bool r0 = row < n, r1 = row + 1 < n;
+    for (int c = tid >> 2; c < cols; c += 8 * kRltWarps) {
       double* dst = ab + ab_idx(c, g2);
-      const bool v0 = row < n && c < n, v1 = row + 1 < n && c < n;
+      const bool v0 = r0 && c < n, v1 = r1 && c < n;
       const double* src = A + rlt_off<PM>(lda, v0 ? row : 0, v0 ? c : 0);
-      if (v1 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+      if (v1 && pair_al) {
         cp_async16(dst, src);
       } else {
         cp_async8(dst, src, v0);
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     return (!PM && L.twin) ? (long long)cc + (long long)rr * ld : rlt_off<PM>(ld, rr, cc);
   };
   bool bad = false;  // this lane saw a non-finite X
+  double wn0 = R.W[p * R.ntmax * 64 + lane], wn1 = R.W[p * R.ntmax * 64 + 32 + lane];  // tile 0's inverse
   double nb0 = (rok && 2 * t < n) ? B[xo(ldb, r, 2 * t)] : 0.0;
   double nb1 = (rok && 2 * t + 1 < n) ? B[xo(ldb, r, 2 * t + 1)] : 0.0;
 #pragma unroll
@@ -239,8 +243,12 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
       const int s0 = (lane & ~3) | (t >> 1), s1 = (lane & ~3) | (2 + (t >> 1));
       const double u00 = __shfl_sync(0xffffffffu, acc0, s0), u01 = __shfl_sync(0xffffffffu, acc1, s0);
       const double u10 = __shfl_sync(0xffffffffu, acc0, s1), u11 = __shfl_sync(0xffffffffu, acc1, s1);
-      const double* w = R.W + (p * R.ntmax + J) * 64 + lane;
-      const double w0 = w[0], w1 = w[32];
+      const double w0 = wn0, w1 = wn1;
+      if (J + 1 < nt) {  // next tile's inverse fragments, loaded under this tile's solve
+        const double* w = R.W + (p * R.ntmax + J + 1) * 64 + lane;
+        wn0 = w[0];
+        wn1 = w[32];
+      }
       acc0 = acc1 = 0.0;
       dmma(acc0, acc1, (t & 1) ? u01 : u00, w0);
       dmma(acc0, acc1, (t & 1) ? u11 : u10, w1);
