@@ -385,8 +385,6 @@ def series_dgemm(S: Series):
             del A, B, C
             continue
         # CPU leg + parity on the first `smp` problems (fresh C for both sides)
-        Cs = torch.rand((batch, n, n), generator=g, device=dev, dtype=torch.float64)[:1]
-        del Cs
         h = [x.cpu().numpy().reshape(batch, -1) for x in (A, B)]
         c0 = (torch.rand((min(batch, 4096), n * n), generator=g, device=dev, dtype=torch.float64) * 2 - 1)
         c0h = c0.cpu().numpy()
@@ -587,8 +585,6 @@ def series_chain(S: Series):
     roof = float(sum(_roof(2 * int(n) ** 3 + int(n) ** 3 // 3, 8 * (3 * int(n) ** 2 + int(n) * (int(n) + 1)),
                            S.peak, S.bw) for n in ns))
     out = {}
-    dn = torch.from_numpy(ns).to(dev)
-    doff = torch.from_numpy(offs).to(dev)
     info = torch.empty(batch, dtype=torch.int32, device=dev)
     for layout in "CP":
         g = torch.Generator(device=dev).manual_seed(50 + (layout == "P"))
