@@ -100,6 +100,15 @@ static bool chain_unfused() {
   return v;
 }
 
+// PBGPU_CHAIN_SYRK=fused: small orders form S in the Cholesky kernel's prologue (A/B only)
+static bool chain_engine_syrk() {
+  static const bool v = [] {
+    const char* e = getenv("PBGPU_CHAIN_SYRK");
+    return !(e && e[0] == 'f');
+  }();
+  return v;
+}
+
 cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
   if (L.batch <= 0) return cudaSuccess;
   mempool_keep();
@@ -159,7 +168,30 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       int* bn = d_n + b0;
       int* binfo = d_info + b0;
       long long* boff = d_off + b0;
-      if (!L.pm && (nmax <= 32 || chain_unfused())) {
+      if (nmax > 32 && chain_engine_syrk()) {
+        // S = C + A A^T per distinct order on the tile engine (per-problem offsets,
+        // bulk-copied operands), then the Cholesky of the class without a prologue
+        for (size_t c0 = b0; c0 < b1 && e == cudaSuccess;) {
+          size_t c1 = c0;
+          while (c1 < b1 && sn[c1] == sn[c0]) ++c1;
+          const int n = sn[c0];
+          bool even = n % 2 == 0;
+          for (size_t q = c0; q < c1; ++q) even = even && so[q] % 2 == 0;
+          GemmLaunch g;
+          g.lay_a = g.lay_b = L.pm ? L_PMX : L_MNC;
+          g.out_pm = L.pm;
+          g.a.base = g.b.base = L.A; g.a.ld = g.b.ld = n; g.a.offs = g.b.offs = d_off + c0;
+          g.a.bulk = g.b.bulk = even && (reinterpret_cast<uintptr_t>(L.A) & 15) == 0;
+          g.o.c = L.C; g.o.d = L.C; g.o.ldc = g.o.ldd = n; g.o.offs = d_off + c0;
+          g.o.vec = even && (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
+          g.m = g.n = g.k = n;
+          g.alpha = 1.0; g.beta = 1.0; g.uplo = 1; g.batch = (int)(c1 - c0);
+          e = gemm_launch(g, s);
+          c0 = c1;
+        }
+        if (e == cudaSuccess)
+          e = potrf_cta_launch(L.C, 0, boff, bn, 0, nmax, 0, L.pm, L.pm, binfo, 0, 0, bs, s);
+      } else if (!L.pm && (nmax <= 32 || chain_unfused())) {
         // register-resident Cholesky for the smallest orders: syrk first, then potrf_reg
         e = syrk_lower_cta_launch(L.C, boff, bn, L.A, nmax, 0, binfo, bs, s);
         if (e == cudaSuccess) e = potrf_cta_launch(L.C, 0, boff, bn, 0, nmax, 0, 0, 0, binfo, 0, 0, bs, s);
