@@ -109,6 +109,15 @@ static bool chain_engine_syrk() {
   return v;
 }
 
+// PBGPU_CHAIN_ENGINE_FROM=n: classes above n use the engine syrk (tuning)
+static int chain_engine_from() {
+  static const int v = [] {
+    const char* e = getenv("PBGPU_CHAIN_ENGINE_FROM");
+    return e ? atoi(e) : 32;
+  }();
+  return v;
+}
+
 cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
   if (L.batch <= 0) return cudaSuccess;
   mempool_keep();
@@ -168,7 +177,7 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       int* bn = d_n + b0;
       int* binfo = d_info + b0;
       long long* boff = d_off + b0;
-      if (nmax > 32 && chain_engine_syrk()) {
+      if (nmax > chain_engine_from() && chain_engine_syrk()) {
         // S = C + A A^T per distinct order on the tile engine (per-problem offsets,
         // bulk-copied operands), then the Cholesky of the class without a prologue
         for (size_t c0 = b0; c0 < b1 && e == cudaSuccess;) {
