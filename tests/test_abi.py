@@ -137,3 +137,75 @@ def test_batched_null_info_rejected(pb):
     P = pb.PanelRef
     r = pb.syrk_potrf_nd_batched(4, 0, P(buf, 4, 0), 0, P(buf, 4, 0), 0, P(buf, 4, 4), 16, P(buf, 4, 4), 16, None, 2)
     assert r.info == -14
+
+
+_SHIM_RUN = r'''
+#include "pbgpu_panelblas.hpp"
+#include "pb_oracle.h"
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+static double relf(const std::vector<double>& a, const std::vector<double>& b) {
+  double num = 0, den = 0;
+  for (size_t i = 0; i < a.size(); ++i) { num += (a[i] - b[i]) * (a[i] - b[i]); den += b[i] * b[i]; }
+  return std::sqrt(num / (den > 0 ? den : 1));
+}
+int main() {
+  std::mt19937_64 rng(7);
+  std::uniform_real_distribution<double> u(-1, 1);
+  pbgpu::BlasConfig cfg;
+  const int n = 48;
+  std::vector<double> A(n * n), B(n * n), C(n * n);
+  for (auto* v : {&A, &B, &C}) for (auto& x : *v) x = u(rng);
+  // dgemm through the reference-shaped signature vs the oracle
+  std::vector<double> c1 = C, c2 = C;
+  auto r = pbgpu::dgemm(cfg, 'n', 't', n, n, n, 1.5, A.data(), n, B.data(), n, -0.5, c1.data(), n);
+  orc_dgemm('n', 't', n, n, n, 1.5, A.data(), n, B.data(), n, -0.5, c2.data(), n);
+  if (!r.ok() || relf(c1, c2) > 1e-13 * n || r.flops != 2LL * n * n * n) { std::printf("dgemm\n"); return 1; }
+  // dpotrf on an SPD matrix
+  std::vector<double> S(n * n, 0.0);
+  for (int i = 0; i < n; ++i) for (int j = 0; j < n; ++j) {
+    for (int l = 0; l < n; ++l) S[i + j * n] += A[i + l * n] * A[j + l * n];
+    if (i == j) S[i + j * n] += n;
+  }
+  std::vector<double> s1 = S, s2 = S;
+  r = pbgpu::dpotrf(cfg, 'l', n, s1.data(), n);
+  if (r.info != 0 || orc_dpotrf('l', n, s2.data(), n) != 0) { std::printf("dpotrf info\n"); return 2; }
+  for (int j = 0; j < n; ++j) for (int i = 0; i < j; ++i) s1[i + j * n] = s2[i + j * n] = 0.0;
+  if (relf(s1, s2) > 1e-13 * n) { std::printf("dpotrf\n"); return 3; }
+  // dgetrf: pivots bit-exact
+  std::vector<double> g1 = A, g2 = A;
+  std::vector<int> p1, p2(n);
+  r = pbgpu::dgetrf(cfg, n, n, g1.data(), n, p1);
+  orc_dgetrf(n, n, g2.data(), n, p2.data());
+  if (r.info != 0 || p1 != p2) { std::printf("dgetrf pivots\n"); return 4; }
+  // argument error in abort mode throws ArgError with the reference's index
+  pbgpu::BlasConfig strict;
+  strict.abort_on_error = true;
+  try { pbgpu::dpotrf(strict, 'x', n, s1.data(), n); return 5; } catch (const pbgpu::ArgError& e) {
+    if (e.index() != 1) return 6;
+  }
+  std::printf("shim ok\n");
+  return 0;
+}
+'''
+
+
+@pytest.mark.gpu
+def test_shim_compute_calls_match_the_oracle(tmp_path, orc):
+    """Compute calls through the reference-shaped C++ signatures (pbgpu_panelblas.hpp) on the
+    GPU: dgemm and dpotrf within 1e-13 n of the oracle, dgetrf pivots bit-exact, ArgError."""
+    import subprocess
+    src = tmp_path / "shim.cpp"
+    src.write_text(_SHIM_RUN)
+    exe = tmp_path / "shim"
+    pkg = os.path.join(ROOT, "paper_1902_08115_b200")
+    obuild = os.path.join(ROOT, "oracle", "_build")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), "-I",
+                        os.path.join(ROOT, "oracle"), str(src), "-o", str(exe),
+                        os.path.join(pkg, "libpbgpu.so"), os.path.join(obuild, "liboracle.so"),
+                        f"-Wl,-rpath,{pkg}:{obuild}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "shim ok" in out.stdout, (out.returncode, out.stdout, out.stderr)
