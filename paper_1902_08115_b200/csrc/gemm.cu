@@ -39,7 +39,15 @@
 namespace pbg {
 
 constexpr int TM = 64, TN = 64, BK = 32;
-constexpr int NCW = 8;  // consumer warps
+#ifndef PB_ENGINE_WH
+#define PB_ENGINE_WH 2
+#endif
+// warp tile: WH row tiles x WF column tiles of 8x8 (of D' = C^T); measured: WH = 4
+// (four 32x32-tile warps, half the fragment loads per DMMA) is 25 % slower than
+// eight 32x16-tile warps (WH = 2) at every compute-bound size
+constexpr int WH = PB_ENGINE_WH, WF = 4;
+constexpr int NWR = TM / (8 * WH);                 // warps along the tile's rows
+constexpr int NCW = NWR * (TN / (8 * WF));         // consumer warps
 constexpr int NTHREADS = (NCW + 1) * 32;
 
 template <int L>
@@ -271,21 +279,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
 
   // -------------------------------------------------------------- consumers
   const int g = lane >> 2, t = lane & 3;
-  const int jb = (warp >> 2) * 32, ib = (warp & 3) * 16;
+  const int jb = (warp / NWR) * 8 * WF, ib = (warp % NWR) * 8 * WH;
   const bool use_c = P.beta != 0.0;
   // beta*C operands for this lane's 4x2 fragments, prefetched one item ahead
   // so their DRAM latency hides behind a whole item of tensor-core work.
-  double cv[4][2][2], cn[4][2][2];
-  auto load_c = [&](long long it, double (&dst)[4][2][2]) {
+  double cv[WF][WH][2], cn[WF][WH][2];
+  auto load_c = [&](long long it, double (&dst)[WF][WH][2]) {
     int p, tm, tn;
     decode_item(P, it, p, tm, tn);
     const double* cbase =
         P.o.c + (P.o.offs_c ? P.o.offs_c[p] : P.o.offs ? P.o.offs[p] : (long long)p * P.o.sc);
     const bool live = !(P.skip && P.skip[p]);
 #pragma unroll
-    for (int f = 0; f < 4; ++f)
+    for (int f = 0; f < WF; ++f)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < WH; ++h) {
         const int i = tm * TM + ib + h * 8 + 2 * t, j = tn * TN + jb + f * 8 + g;
         dst[f][h][0] = dst[f][h][1] = 0.0;
         if (j < P.n && live) {
@@ -309,20 +317,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
     decode_item(P, item, p, tm, tn);
     if (use_c) {
 #pragma unroll
-      for (int f = 0; f < 4; ++f)
+      for (int f = 0; f < WF; ++f)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) { cv[f][h][0] = cn[f][h][0]; cv[f][h][1] = cn[f][h][1]; }
+        for (int h = 0; h < WH; ++h) { cv[f][h][0] = cn[f][h][0]; cv[f][h][1] = cn[f][h][1]; }
       if (item + gridDim.x < P.items) load_c(item + gridDim.x, cn);
     }
     if (P.skip && P.skip[p]) continue;
     const int i0 = tm * TM, j0 = tn * TN;
     double* dbase = P.o.d + (P.o.offs ? P.o.offs[p] : (long long)p * P.o.sd);
 
-    double acc[4][2][2];
+    double acc[WF][WH][2];
 #pragma unroll
-    for (int f = 0; f < 4; ++f)
+    for (int f = 0; f < WF; ++f)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) acc[f][h][0] = acc[f][h][1] = 0.0;
+      for (int h = 0; h < WH; ++h) acc[f][h][0] = acc[f][h][1] = 0.0;
 
     for (int kc = 0; kc < P.nk; ++kc) {
       const int kvalid = min(BK, P.k - kc * BK);
@@ -333,15 +341,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
           const int l = ks * 4 + t;
-          double av[4], bv[2];
+          double av[WF], bv[WH];
 #pragma unroll
-          for (int f = 0; f < 4; ++f) av[f] = sB[TB::at(jb + f * 8 + g, l)];
+          for (int f = 0; f < WF; ++f) av[f] = sB[TB::at(jb + f * 8 + g, l)];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) bv[h] = sA[TA::at(ib + h * 8 + g, l)];
+          for (int h = 0; h < WH; ++h) bv[h] = sA[TA::at(ib + h * 8 + g, l)];
 #pragma unroll
-          for (int f = 0; f < 4; ++f)
+          for (int f = 0; f < WF; ++f)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
+            for (int h = 0; h < WH; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
         }
       } else {
         // Tail chunk: lanes past k contribute exact zeros whatever the stage
@@ -350,15 +358,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
         for (int ks = 0; ks < ksteps; ++ks) {
           const int l = ks * 4 + t;
           const bool in = l < kvalid;
-          double av[4], bv[2];
+          double av[WF], bv[WH];
 #pragma unroll
-          for (int f = 0; f < 4; ++f) av[f] = in ? sB[TB::at(jb + f * 8 + g, l)] : 0.0;
+          for (int f = 0; f < WF; ++f) av[f] = in ? sB[TB::at(jb + f * 8 + g, l)] : 0.0;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) bv[h] = in ? sA[TA::at(ib + h * 8 + g, l)] : 0.0;
+          for (int h = 0; h < WH; ++h) bv[h] = in ? sA[TA::at(ib + h * 8 + g, l)] : 0.0;
 #pragma unroll
-          for (int f = 0; f < 4; ++f)
+          for (int f = 0; f < WF; ++f)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
+            for (int h = 0; h < WH; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
         }
       }
       __syncwarp();
@@ -368,9 +376,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
 
     // Epilogue: d = alpha*acc + beta*c, masked to the problem and the uplo triangle.
 #pragma unroll
-    for (int f = 0; f < 4; ++f)
+    for (int f = 0; f < WF; ++f)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < WH; ++h) {
         const int i = i0 + ib + h * 8 + 2 * t, j = j0 + jb + f * 8 + g;
         if (j >= P.n) continue;
         double r0 = use_c ? fma(P.alpha, acc[f][h][0], P.beta * cv[f][h][0]) : acc[f][h][0] * P.alpha;
