@@ -298,6 +298,116 @@ __global__ void __launch_bounds__(32 * T * SPL) gemm_mid_kernel(const __grid_con
   if (SC && tid == 0) bulk_wait_read0();
 }
 
+// 84 <= s <= 96 (T = 11, 12): one problem does not fit twice in shared memory,
+// so the operands stream in two k halves (columns [0, k0) and [k0, s) of every
+// panel, k0 = 4 floor(s / 8)) into two slots: while one half is multiplied the
+// other half — and then the next problem's first half — is in flight.  One
+// bulk copy per panel and operand (issued by one thread), C prefetched into
+// registers when the problem starts, D straight from the accumulators.
+template <int T>
+__global__ void __launch_bounds__(32 * T, 1) gemm_midk_kernel(const __grid_constant__ SmallArgs P) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[2];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int s = P.s, k0 = 4 * (s / 8), kh[2] = {k0, s - k0}, kmax = max(kh[0], kh[1]);
+  const long long ss = (long long)s * s;
+  const bool use_c = P.beta != 0.0;
+  const int np = s / 4;  // panels per operand
+  auto slot = [&](int h) { return sm + (size_t)h * 2 * s * kmax; };
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long prob, int h) {  // tid 0: half h of problem prob into slot h
+    const int kc = kh[h], c0 = h ? k0 : 0;
+    const uint32_t bytes = 32u * (uint32_t)kc;  // one panel's 4 rows x kc columns
+    mbar_arrive_expect_tx(&full[h], 2u * (uint32_t)np * bytes);
+    for (int o = 0; o < 2; ++o) {
+      const double* src = (o ? P.b : P.a) + prob * ss + 4 * c0;
+      double* dst = slot(h) + (size_t)o * s * kmax;
+      for (int q = 0; q < np; ++q) bulk_g2s(dst + (size_t)q * 4 * kc, src + (long long)q * 4 * s, bytes, &full[h]);
+    }
+  };
+  long long prob = blockIdx.x;
+  if (tid == 0 && prob < P.batch) {
+    issue(prob, 0);
+    issue(prob, 1);
+  }
+  const int I = warp, ra = 8 * I + g;
+  for (int it = 0; prob < P.batch; prob += gridDim.x, ++it) {
+    const long long next = prob + gridDim.x;
+    const double* Cg = P.c + prob * ss;
+    double* Dg = P.d + prob * ss;
+    double cpre[T][2];  // C loaded before the k loop so its latency hides under it
+#pragma unroll
+    for (int J = 0; J < T; ++J)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+        cpre[J][e] = ldg_if(Cg + (long long)(r >> 2) * 4 * s + c * 4 + (r & 3), use_c && r < s && c < s, 0.0);
+      }
+    double acc[T][2];
+#pragma unroll
+    for (int J = 0; J < T; ++J) acc[J][0] = acc[J][1] = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mbar_wait(&full[h], (uint32_t)(it & 1));
+      const double* A = slot(h);
+      const double* B = A + (size_t)s * kmax;
+      const int kc = kh[h];
+      // element (r, c) of a half: (r/4) * 4 kc + 4 c + r%4; rows past s read the
+      // neighbouring data / slack and only feed discarded outputs
+      for (int l0 = 0; l0 < kc; l0 += 4) {
+        const double fa = A[(ra >> 2) * 4 * kc + (l0 + t) * 4 + (ra & 3)];
+        double fb[T];
+#pragma unroll
+        for (int J = 0; J < T; ++J) {
+          const int rb = 8 * J + g;
+          fb[J] = B[(rb >> 2) * 4 * kc + (l0 + t) * 4 + (rb & 3)];
+        }
+#pragma unroll
+        for (int J = 0; J < T; ++J) dmma(acc[J][0], acc[J][1], fa, fb[J]);
+      }
+      __syncthreads();  // every warp is done with slot h
+      if (tid == 0 && next < P.batch) issue(next, h);
+    }
+#pragma unroll
+    for (int J = 0; J < T; ++J)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * I + g, c = 8 * J + 2 * t + e;
+        if (r < s && c < s)
+          Dg[(long long)(r >> 2) * 4 * s + c * 4 + (r & 3)] =
+              use_c ? fma(P.alpha, acc[J][e], P.beta * cpre[J][e]) : P.alpha * acc[J][e];
+      }
+  }
+}
+
+template <int T>
+static cudaError_t midk_t(SmallArgs& P, cudaStream_t st) {
+  const int s = P.s, k0 = 4 * (s / 8), kmax = std::max(k0, s - k0);
+  // two slots of A and B halves + one panel chunk of slack for the last tile's rows past s
+  const size_t smem = ((size_t)2 * 2 * s * kmax + 4 * (size_t)kmax) * sizeof(double);
+  {
+    cudaError_t e = smem_attr((const void*)gemm_midk_kernel<T>, 220 * 1024);
+    if (e != cudaSuccess) return e;
+  }
+  const int grid = (int)std::min<long long>(P.batch, (long long)num_sms());
+  gemm_midk_kernel<T><<<grid, 32 * T, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+// PBGPU_GEMM_MIDK=0: the single-stage row-tile kernel above s = 80 (A/B only)
+static bool midk_on() {
+  static const bool v = [] {
+    const char* e = getenv("PBGPU_GEMM_MIDK");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 template <int T, bool SC, int NST, int SPL = (T <= 8 ? 2 : 1)>
 static cudaError_t mid_t(SmallArgs& P, cudaStream_t st) {
   // + one 4-row panel of slack: the last tile's rows past s read (and discard) past the last operand
@@ -326,6 +436,13 @@ static cudaError_t mid_launch(SmallArgs& P, cudaStream_t st) {
     switch ((s + 7) / 8) {
       case 9: return mid_t<9, false, 2>(P, st);
       case 10: return mid_t<10, false, 2>(P, st);
+    }
+  } else if (midk_on() && s <= 96) {
+    // (13-14 warps are capped at 128 registers and spill the C prefetch: measured
+    // 0.76-0.93x there, so s = 100..112 stay on the single-stage kernel)
+    switch ((s + 7) / 8) {
+      case 11: return midk_t<11>(P, st);
+      case 12: return midk_t<12>(P, st);
     }
   } else {
     switch ((s + 7) / 8) {
