@@ -68,6 +68,9 @@ struct PotrfCtaArgs {
   CUtensorMap tm[kCtaMaxT];
 };
 
+#ifndef PB_REDUNDANT_FROM  // panels factored with the redundant diagonal block from T = 9 (n = 72) on
+#define PB_REDUNDANT_FROM 9
+#endif
 #ifndef PB_CTA_PAD
 #define PB_CTA_PAD 4
 #endif
@@ -496,7 +499,7 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
       // that, rows per lane follow the panel's height (fewer predicated-off rows)
       const uint32_t pk = sbase + 8u * cta_pbase(T, k), cbuf = smem_u32(&sh_col[0][0]);
       int f;
-      if constexpr (T >= 9) {
+      if constexpr (T >= PB_REDUNDANT_FROM) {
         f = cta_factor_panel<R>(pk, RS, rows, lane, 8 * k, n);  // (rows-following measured slower here)
       } else if constexpr (R > 1) {
         if (rows <= 32) f = cta_factor_panel_bc<1>(pk, RS, rows, lane, 8 * k, n, cbuf);
