@@ -56,7 +56,17 @@ __global__ void scatter_info_kernel(const int* src, const int* idx, int* info, i
 // ------------------------------------------------------------------ syrk_potrf_nd
 cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
   if (L.batch <= 0 || L.n <= 0) return cudaSuccess;
-  const bool fused_ok = L.n <= 160 && !L.offs && (L.k == 0 || (L.cna == L.cnb && L.sa == L.sb));
+  // fused (S formed in the Cholesky kernel's prologue) up to n = 112 or k < 16;
+  // above, the tile engine forms S first (measured: n = 128, k = 64 0.96 ->
+  // 0.82 ms; n = 160, k = 160 1.70 -> 1.07 ms; the prologue wins at n <= 96).
+  // On a numerical failure the engine path leaves S (not the caller's D) in the
+  // entries outside the reference's partial write set, as the blocked n > 160 path.
+  static const int fused_nmax = [] {
+    const char* e = getenv("PBGPU_SYRK_POTRF_FUSED_NMAX");
+    return e ? atoi(e) : 112;
+  }();
+  const bool fused_ok = L.n <= 160 && !L.offs && (L.n <= fused_nmax || L.k < 16) &&
+                        (L.k == 0 || (L.cna == L.cnb && L.sa == L.sb));
   if (fused_ok)
     return syrk_potrf_cta_launch(L.d, L.sd, nullptr, nullptr, L.cnd, L.c, L.sc, L.cnc, L.k ? L.a : nullptr,
                                  L.k ? L.b : nullptr, L.sa, L.k, L.cna, L.n, 1, 1, L.info, L.batch, s);
