@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -145,6 +146,8 @@ struct Operand {
 };
 
 // Per-thread staging resources for host-pointer calls (per device).
+// Host-pointer staging state: per calling thread AND per device (a thread that
+// drives several GPUs keeps one set of streams and buffers on each).
 struct Stager {
   int device = -1;
   cudaStream_t st[2] = {nullptr, nullptr};
@@ -152,19 +155,18 @@ struct Stager {
   std::vector<size_t> caps[2];
   ~Stager() {
     // Process teardown may already have destroyed the context: ignore errors.
-    for (int s = 0; s < 2; ++s)
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (device >= 0) cudaSetDevice(device);
+    for (int s = 0; s < 2; ++s) {
       for (void* b : bufs[s]) cudaFree(b);
+      if (st[s]) cudaStreamDestroy(st[s]);
+    }
+    if (cur >= 0) cudaSetDevice(cur);
     cudaGetLastError();
   }
   cudaError_t ensure(int dev, size_t nops) {
-    if (device != dev) {
-      for (int s = 0; s < 2; ++s) {
-        bufs[s].clear();
-        caps[s].clear();
-        st[s] = nullptr;
-      }
-      device = dev;
-    }
+    device = dev;
     for (int s = 0; s < 2; ++s) {
       if (!st[s]) {
         cudaError_t e = cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking);
@@ -191,7 +193,7 @@ struct Stager {
     return cudaSuccess;
   }
 };
-thread_local Stager g_stager;
+thread_local std::map<int, Stager> g_stagers;  // device -> this thread's staging state
 
 size_t region_bytes(const Operand& o, long long nb) {
   if (nb <= 0 || o.extent <= 0) return 0;
@@ -232,7 +234,7 @@ int run_batched(const char* routine, std::vector<Operand> ops, int batch, pb_str
   }
   int dev = 0;
   cudaGetDevice(&dev);
-  Stager& S = g_stager;
+  Stager& S = g_stagers[dev];
   cudaError_t e = S.ensure(dev, ops.size());
   if (e != cudaSuccess) return cuda_fail(res, routine, e);
   size_t per = 0;

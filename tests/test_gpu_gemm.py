@@ -250,3 +250,39 @@ def test_gemm_nd_cfg2_full_batch(pb, cuda, s):
     want = dense(A) @ dense(B).transpose(1, 2) + dense(C)
     err = (torch.linalg.matrix_norm(dense(D) - want) / torch.linalg.matrix_norm(want)).max().item()
     assert err <= tol(s)
+
+
+def test_host_pointer_calls_from_concurrent_threads(pb, orc):
+    """§8(b) threading: host-pointer calls from several threads at once (each thread has its
+    own staging streams and buffers) all match the oracle."""
+    import threading
+    rng = np.random.default_rng(42)
+    m = n = k = 40
+    batch = 600
+    jobs = []
+    for _ in range(4):
+        A = rng.uniform(-1, 1, (batch, k, m)); B = rng.uniform(-1, 1, (batch, n, k)); C = rng.uniform(-1, 1, (batch, n, m))
+        jobs.append([A, B, C, C.copy()])
+    errors = []
+
+    def work(job):
+        try:
+            A, B, C, out = job
+            for _ in range(3):
+                out[:] = C
+                r = pb.dgemm_batched("n", "n", m, n, k, 1.0, A, m, m * k, B, k, k * n, 1.0, out, m, m * n, batch)
+                assert r.ok(), r
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(j,)) for j in jobs]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for A, B, C, out in jobs:
+        want = C.copy()
+        orc.dgemm_batch(b"n", b"n", m, n, k, 1.0, A.ctypes.data, m, m * k, B.ctypes.data, k, k * n, 1.0,
+                        want.ctypes.data, m, m * n, batch, 4)
+        assert rel_frob(out, want) <= tol(k)
