@@ -217,6 +217,8 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
   }();
   if (!legacy && getrf_reg_ok(L.m, L.n))
     return getrf_reg_launch(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, L.batch, s);
+  if (!legacy && getrf_sq_ok(L.a, L.stride, L.lda, L.m, L.n))
+    return getrf_sq_launch(L.a, L.stride, L.lda, L.n, L.ipiv, L.stride_ipiv, L.info, L.batch, s);
   static const int blocked_from = [] {  // PBGPU_GETRF_BLOCKED_FROM=n: blocked path from this order on (tuning)
     const char* e = getenv("PBGPU_GETRF_BLOCKED_FROM");
     return e ? atoi(e) : 80;

@@ -126,12 +126,53 @@ __global__ void k(double* out, long long* cyc, double x0) {
   }
   t1 = clock64(); cyc[11] = t1 - t0;
   acc += pidx;
+  // redux.sync (CREDUX) chain: max over the warp feeding the next input
+  unsigned ru = threadIdx.x * 2654435761u;
+  t0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < 256; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ru = __reduce_max_sync(0xffffffffu, ru) ^ (threadIdx.x + j);
+  }
+  t1 = clock64(); cyc[12] = t1 - t0;
+  // ballot chain
+  t0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < 256; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ru = __ballot_sync(0xffffffffu, (ru >> (threadIdx.x & 7)) & 1) + threadIdx.x + j;
+  }
+  t1 = clock64(); cyc[13] = t1 - t0;
+  // sts.128 -> syncwarp -> lds.128 round trip (one lane publishes, all read)
+  __shared__ __align__(16) double rb[2][4];
+  double rx = x, ry = x + 1.0;
+  t0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < 256; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (threadIdx.x == ((i + j) & 31)) asm volatile("st.shared.v2.f64 [%0], {%1,%2};\n" ::"r"((unsigned)__cvta_generic_to_shared(&rb[j & 1][0])), "d"(rx), "d"(ry) : "memory");
+      __syncwarp();
+      asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(rx), "=d"(ry) : "r"((unsigned)__cvta_generic_to_shared(&rb[j & 1][0])) : "memory");
+      rx += 1.0;
+    }
+  }
+  t1 = clock64(); cyc[14] = t1 - t0;
+  // __drcp_rn chain
+  t0 = clock64();
+#pragma unroll 1
+  for (int i = 0; i < 256; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x = __drcp_rn(x) + 0.5;
+  }
+  t1 = clock64(); cyc[15] = t1 - t0;
+  acc += ru + rx + ry;
   out[threadIdx.x] = x + s + d0 + d1 + acc;
 }
 int main() {
   double* o; long long* c; cudaMalloc(&o, 8 * 32); cudaMallocManaged(&c, 8 * 16);
   k<<<1, 32>>>(o, c, 1.5); cudaDeviceSynchronize();
   k<<<1, 32>>>(o, c, 1.5); cudaDeviceSynchronize();
-  const char* nm[] = {"dfma", "dmul", "rsqrt(double)", "rsqrtf+2NR", "sqrt(double)", "1/x", "shfl", "dadd", "dmma dep", "dmma 8 indep", "rsqrt_nb", "lds chain"};
-  for (int i = 0; i < 12; ++i) printf("%-16s %6.1f cycles/op\n", nm[i], c[i] / 2048.0);
+  const char* nm[] = {"dfma", "dmul", "rsqrt(double)", "rsqrtf+2NR", "sqrt(double)", "1/x", "shfl", "dadd", "dmma dep", "dmma 8 indep", "rsqrt_nb", "lds chain", "redux.max (CREDUX)", "ballot", "sts128+syncwarp+lds128 (+dadd)", "__drcp_rn (+dadd)"};
+  for (int i = 0; i < 16; ++i) printf("%-32s %6.1f cycles/op\n", nm[i], c[i] / 2048.0);
 }

@@ -4,6 +4,8 @@
 //      tools/potrf_trace.cu -o tools/potrf_trace
 #define PB_TRACE 1
 #include "../paper_1902_08115_b200/csrc/potrf_cta.cu"
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <vector>
 
@@ -45,6 +47,31 @@ int main(int argc, char** argv) {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     printf("rep %d: %.4f ms (%s)\n", rep, ms, cudaGetErrorString(cudaGetLastError()));
+  }
+  {  // residual ||L L^T - A||_F / ||A||_F on a few problems
+    std::vector<double> L((size_t)n * n), A((size_t)n * n);
+    std::vector<int> inf(batch);
+    cudaMemcpy(inf.data(), info, sizeof(int) * batch, cudaMemcpyDeviceToHost);
+    int bad = 0;
+    for (int i = 0; i < batch; ++i) bad += inf[i] != 0;
+    double worst = 0.0;
+    const int probes[4] = {0, 1, batch / 2, batch - 1};
+    for (int q = 0; q < 4; ++q) {
+      const size_t o = (size_t)probes[q] * n * n;
+      cudaMemcpy(L.data(), a + o, sizeof(double) * n * n, cudaMemcpyDeviceToHost);
+      cudaMemcpy(A.data(), a0 + o, sizeof(double) * n * n, cudaMemcpyDeviceToHost);
+      double num = 0.0, den = 0.0;
+      for (int c = 0; c < n; ++c)
+        for (int r = c; r < n; ++r) {
+          double v = 0.0;
+          for (int l = 0; l <= c; ++l) v += L[r + (size_t)l * n] * L[c + (size_t)l * n];
+          const double d = v - A[r + (size_t)c * n];
+          num += d * d;
+          den += A[r + (size_t)c * n] * A[r + (size_t)c * n];
+        }
+      worst = std::max(worst, std::sqrt(num / den));
+    }
+    printf("check: nonzero info %d, worst residual %.3e\n", bad, worst);
   }
   std::vector<long long> tr(256 * 64);
   cudaMemcpyFromSymbol(tr.data(), pbg::pb_trace, sizeof(long long) * tr.size());
