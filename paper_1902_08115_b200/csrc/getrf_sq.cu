@@ -60,7 +60,8 @@ __device__ __forceinline__ void sq_sync(int id, int count) {
 // in registers with virtual interchanges, write it back at the final positions
 // and record the pivots.  Returns the updated first-zero column (1-based, 0 = none).
 template <int T, int RK>
-__device__ __forceinline__ int sq_panel(uint32_t sbase, int c0, int lane, uint32_t scr, int* piv_all, int fz) {
+__device__ __forceinline__ int sq_panel(uint32_t sbase, int c0, int lane, uint32_t scr, int* piv_all, int* mv,
+                                        int fz) {
   constexpr int N = 8 * T, S = sq_stride(T);
   double x[RK][8];
   int pos[RK];
@@ -138,8 +139,12 @@ __device__ __forceinline__ int sq_panel(uint32_t sbase, int c0, int lane, uint32
       }
     }
   }
-  // rows at their final positions (the positions are a permutation of the rows)
+  // rows at their final positions (the positions are a permutation of the rows),
+  // and the block's interchanges composed into a move list for the other
+  // columns: mv[1 + i] = src | dst << 16 for every row whose position changed
+  // (at most 16: eight pivot rows up, the rows they displaced down), mv[0] = count
   const uint32_t colb = sbase + 8u * (uint32_t)(c0 * S);
+  int base = 0;
 #pragma unroll
   for (int q = 0; q < RK; ++q) {
     const int r = c0 + lane + 32 * q;
@@ -148,35 +153,103 @@ __device__ __forceinline__ int sq_panel(uint32_t sbase, int c0, int lane, uint32
 #pragma unroll
       for (int c = 0; c < 8; ++c) sts64(d + 8u * (uint32_t)(c * S), x[q][c]);
     }
+    const bool moved = r < N && pos[q] != r;
+    const unsigned m = __ballot_sync(0xffffffffu, moved);
+    if (moved) mv[1 + base + __popc(m & ((1u << lane) - 1u))] = r | (pos[q] << 16);
+    base += __popc(m);
   }
+  if (lane == 0) mv[0] = base;
   return fz;
 }
 
-// Update warps, step 1 for columns [j0, j1) (swap_only: interchanges alone):
-// block k's interchanges in pivot order, then the unit-lower solve against
-// L11, one thread per column.
+// Update warps: block k's interchanges on the 8 columns of tile J, as the
+// composed move list (all loads, then all stores).  Lane = column (lane & 7) x
+// move slot (lane >> 3); up to 16 moves.
+template <int T>
+__device__ __forceinline__ void sq_tile_moves(uint32_t sbase, int J, const int* mv, int lane) {
+  constexpr int S = sq_stride(T);
+  const int cnt = mv[0];
+  if (cnt == 0) return;  // warp-uniform
+  const uint32_t colb = sbase + 8u * (uint32_t)((8 * J + (lane & 7)) * S);
+  const int s = lane >> 3;
+  double v[4];
+  int dst[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = s + 4 * i;
+    const int e = m < cnt ? mv[1 + m] : 0;
+    dst[i] = e >> 16;
+    v[i] = m < cnt ? lds64(colb + 8u * (uint32_t)(e & 0xffff)) : 0.0;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (s + 4 * i < cnt) sts64(colb + 8u * (uint32_t)dst[i], v[i]);
+  __syncwarp();
+}
+
+// inv(L11) of block k (unit lower 8x8): lane j < 8 solves column j against e_j;
+// mbuf[col * 8 + row] (the layout of the DMMA A fragments below)
+template <int T>
+__device__ __forceinline__ void sq_inverse(uint32_t sbase, int c0, uint32_t mbuf, int lane) {
+  constexpr int S = sq_stride(T);
+  if (lane >= 8) return;
+  const uint32_t lb = sbase + 8u * (uint32_t)(c0 + c0 * S);  // L11
+  double y[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double sacc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int l = 0; l < i; ++l) sacc = fma(-lds64(lb + 8u * (uint32_t)(i + l * S)), y[l], sacc);
+    y[i] = sacc;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; i += 2) sts128(mbuf + 8u * (uint32_t)(lane * 8 + i), y[i], y[i + 1]);
+}
+
+// U12 tile J: U(k,J) = inv(L11) A(k,J) on DMMA.  A tile whose result is not
+// finite (Inf/NaN operands, overflow: 0 * Inf of the explicit inverse would
+// differ from the reference's substitution, factor.hpp:188-199) is redone by
+// that substitution, one lane per column.
+template <int T>
+__device__ __forceinline__ void sq_tile_solve(uint32_t sbase, int c0, int J, uint32_t mbuf, int lane, int g,
+                                              int t) {
+  constexpr int S = sq_stride(T);
+  const uint32_t bcol = sbase + 8u * (uint32_t)(c0 + t + (8 * J + g) * S);
+  const double b0 = lds64(bcol), b1 = lds64(bcol + 32);
+  const double m0 = lds64(mbuf + 8u * (uint32_t)(t * 8 + g)), m1 = lds64(mbuf + 8u * (uint32_t)((4 + t) * 8 + g));
+  double d0 = 0.0, d1 = 0.0;
+  dmma(d0, d1, m0, b0);
+  dmma(d0, d1, m1, b1);
+  const bool fin = fabs(d0) <= 1.7976931348623157e308 && fabs(d1) <= 1.7976931348623157e308;
+  if (__all_sync(0xffffffffu, fin)) {
+    const uint32_t dcol = sbase + 8u * (uint32_t)(c0 + g + (8 * J + 2 * t) * S);
+    sts64(dcol, d0);
+    sts64(dcol + 8u * S, d1);
+  } else if (lane < 8) {
+    const uint32_t ub = sbase + 8u * (uint32_t)(c0 + (8 * J + lane) * S);
+    const uint32_t lb = sbase + 8u * (uint32_t)(c0 + c0 * S);
+    double u[8];
+#pragma unroll
+    for (int c = 0; c < 8; c += 2) lds128(ub + 8u * c, u[c], u[c + 1]);
+#pragma unroll
+    for (int c = 1; c < 8; ++c)
+#pragma unroll
+      for (int l = 0; l < c; ++l) u[c] -= u[l] * lds64(lb + 8u * (uint32_t)(c + l * S));
+#pragma unroll
+    for (int c = 0; c < 8; c += 2) sts128(ub + 8u * c, u[c], u[c + 1]);
+  }
+  __syncwarp();
+}
+
+// Exact unit-lower solve of U12 for columns [j0, j1) against L11 (factor.hpp:188-199),
+// one thread per column (the look-ahead tile; its interchanges are already applied).
 template <int T, int NU>
-__device__ __forceinline__ void sq_swap_solve(uint32_t sbase, int c0, const int* piv_all, int j0, int j1,
-                                              bool swap_only, int utid) {
+__device__ __forceinline__ void sq_swap_solve(uint32_t sbase, int c0, const int* piv_all, int j0, int j1, int utid) {
   constexpr int S = sq_stride(T), NUT = 32 * NU;
-  if (j0 + utid >= j1) return;
-  int pr[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) pr[c] = piv_all[c0 + c];
+  (void)piv_all;
   for (int j = j0 + utid; j < j1; j += NUT) {
-    const uint32_t colb = sbase + 8u * (uint32_t)(j * S);
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int row = c0 + c;
-      if (pr[c] != row) {
-        const uint32_t ar = colb + 8u * (uint32_t)row, ap = colb + 8u * (uint32_t)pr[c];
-        const double xr = lds64(ar), xp = lds64(ap);
-        sts64(ar, xp);
-        sts64(ap, xr);
-      }
-    }
-    if (swap_only) continue;
-    const uint32_t ub = colb + 8u * (uint32_t)c0;
+    const uint32_t ub = sbase + 8u * (uint32_t)(c0 + j * S);
     const uint32_t lb = sbase + 8u * (uint32_t)(c0 + c0 * S);  // L11
     double u[8];
 #pragma unroll
@@ -240,6 +313,8 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
   extern __shared__ __align__(16) double sm[];
   __shared__ int piv_all[N];                  // 0-based pivot row of every column
   __shared__ __align__(16) double scr[2][10];  // pivot row broadcast: 8 values, reciprocal, position
+  __shared__ int mvl[2][20];                   // composed interchanges of block k (double-buffered)
+  __shared__ __align__(16) double minv[64];    // inv(L11) of the current block
   __shared__ int first_zero;
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -267,33 +342,45 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
       if (k > 0) sq_sync(2, NTH);  // block k fully updated
       const int c0 = 8 * k;
       const int rk = (N - c0 + 31) >> 5;  // rows per lane follow the remaining height
-      if (R >= 3 && rk == 3) fz = sq_panel<T, (R >= 3 ? 3 : 1)>(sbase, c0, lane, scr0, piv_all, fz);
-      else if (R >= 2 && rk == 2) fz = sq_panel<T, (R >= 2 ? 2 : 1)>(sbase, c0, lane, scr0, piv_all, fz);
-      else fz = sq_panel<T, 1>(sbase, c0, lane, scr0, piv_all, fz);
+      int* mv = mvl[k & 1];
+      if (R >= 3 && rk == 3) fz = sq_panel<T, (R >= 3 ? 3 : 1)>(sbase, c0, lane, scr0, piv_all, mv, fz);
+      else if (R >= 2 && rk == 2) fz = sq_panel<T, (R >= 2 ? 2 : 1)>(sbase, c0, lane, scr0, piv_all, mv, fz);
+      else fz = sq_panel<T, 1>(sbase, c0, lane, scr0, piv_all, mv, fz);
       sq_sync(1, NTH);  // panel k and its pivots published
     }
     if (lane == 0) first_zero = fz;
   } else {
     // ---------------------------------------------------------------- update warps
-    const int utid = tid - 32, uw = warp - 1, g = lane >> 2, t = lane & 3;
+    const int uw = warp - 1, g = lane >> 2, t = lane & 3;
+    const uint32_t mbuf = smem_u32(&minv[0]);
     for (int k = 0; k < T; ++k) {
       sq_sync(1, NTH);  // panel k published
       const int c0 = 8 * k, ti = T - k - 1;  // row tiles below the block
+      const int* mv = mvl[k & 1];
       if (k + 1 < T) {
-        // look-ahead: block k+1's columns first, row tiles split across the warps
-        sq_swap_solve<T, NU>(sbase, c0, piv_all, c0 + 8, c0 + 16, false, utid);
+        // look-ahead: tile k+1 first (update warp 0 moves and solves it by the
+        // exact substitution, no wait for the inverse), row tiles split across the warps
+        if (uw == 0) {
+          sq_tile_moves<T>(sbase, k + 1, mv, lane);
+          sq_swap_solve<T, 1>(sbase, c0, piv_all, c0 + 8, c0 + 16, lane);
+        }
         if (NU > 1) sq_sync(3, 32 * NU);
         else __syncwarp();
         sq_tile_col<T>(sbase, c0, k + 1, uw, NU, ti, g, t);
         sq_sync(2, NTH);  // block k+1 ready for the panel warp
-        // the rest: interchanges on the left columns, solve and update right of block k+1
-        sq_swap_solve<T, NU>(sbase, c0, piv_all, c0 + 16, N, false, utid);
-        sq_swap_solve<T, NU>(sbase, c0, piv_all, 0, c0, true, utid);
+        // the rest: inv(L11), then per column tile the interchanges (left tiles
+        // too), the DMMA solve and the trailing update
+        if (uw == 0) sq_inverse<T>(sbase, c0, mbuf, lane);
+        for (int J = uw; J < k; J += NU) sq_tile_moves<T>(sbase, J, mv, lane);
         if (NU > 1) sq_sync(3, 32 * NU);
         else __syncwarp();
-        for (int J = k + 2 + uw; J < T; J += NU) sq_tile_col<T>(sbase, c0, J, 0, 1, ti, g, t);
+        for (int J = k + 2 + uw; J < T; J += NU) {
+          sq_tile_moves<T>(sbase, J, mv, lane);
+          sq_tile_solve<T>(sbase, c0, J, mbuf, lane, g, t);
+          sq_tile_col<T>(sbase, c0, J, 0, 1, ti, g, t);
+        }
       } else {
-        sq_swap_solve<T, NU>(sbase, c0, piv_all, 0, c0, true, utid);
+        for (int J = uw; J < k; J += NU) sq_tile_moves<T>(sbase, J, mv, lane);
       }
     }
   }
