@@ -24,11 +24,19 @@
 //   * Zero pivot: first failing column recorded, no swap, no scaling
 //     (157-158); zero multipliers skip only the rest of their nr = 4 column
 //     group (160-165).
-//   * Update warps: the block's interchanges on the other columns (left ones
-//     too, eagerly), the unit-lower solve of U12 (188-199) one thread per
-//     column, and A22 -= L21 U12 accumulated straight into the C tiles on
-//     DMMA.  Block k+1's columns go first and are handed to the panel warp
-//     (look-ahead), row tiles split across the update warps.
+//   * Update warps, per 8-column tile: the block's interchanges (175-183) as
+//     ONE composed move list (<= 16 rows change position per block: all loads,
+//     then all stores — no dependent swap chain; left tiles too, eagerly), the
+//     unit-lower solve of U12 (188-199) as inv(L11) A12 on DMMA with the exact
+//     substitution for any tile whose result is not finite (the explicit
+//     inverse would turn 0 * Inf into NaN where the reference never multiplies),
+//     and A22 -= L21 U12 accumulated straight into the C tiles on DMMA.  Tile
+//     k+1 goes first (exact substitution, no wait for the inverse) and is
+//     handed to the panel warp (look-ahead), row tiles split across the warps.
+// Measured (tools/getrf_trace.cu): the panel warp is the critical path at
+// ~800-1000 cycles per column under load (460 alone); splitting it over one
+// warp per 32 rows, and a one-redux pivot search with the reciprocal pinned
+// ahead of it, were both neutral (profiles/r02_experiments).
 #include <cstdint>
 #include <cstdlib>
 
@@ -44,6 +52,8 @@ struct GetrfSqArgs {
   int* ipiv;
   long long sp;
   int* info;
+  int piv_offset;  // added to the recorded pivots / failing column (trailing block of the blocked path)
+  int keep_info;   // keep an info already set by an earlier panel
 };
 
 __host__ __device__ constexpr int sq_stride(int T) {  // = 4 mod 16 doubles: conflict-free DMMA fragments
@@ -51,6 +61,15 @@ __host__ __device__ constexpr int sq_stride(int T) {  // = 4 mod 16 doubles: con
   const int s = ((r - 4 + 15) / 16) * 16 + 4;
   return s < r ? s + 16 : s;
 }
+
+// PB_SQ_TRACE (tools/getrf_trace.cu only): clock64 stamps of the phases of a few CTAs
+#ifdef PB_SQ_TRACE
+__device__ long long sq_trace[128][128];
+#define SQ_STAMP(slot) \
+  if ((blockIdx.x & 63) == 0 && (blockIdx.x >> 6) < 128 && (slot) < 128) sq_trace[blockIdx.x >> 6][slot] = clock64();
+#else
+#define SQ_STAMP(slot)
+#endif
 
 __device__ __forceinline__ void sq_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
@@ -321,6 +340,7 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
   const long long p = blockIdx.x;
   double* a = P.a + p * P.stride;
   const uint32_t sbase = smem_u32(sm);
+  if (tid == 0) { SQ_STAMP(0) }
 
   // ---- stage: one TMA bulk copy per column ----
   if (tid == 0) {
@@ -340,12 +360,14 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
     const uint32_t scr0 = smem_u32(&scr[0][0]);
     for (int k = 0; k < T; ++k) {
       if (k > 0) sq_sync(2, NTH);  // block k fully updated
+      if (tid == 0) { SQ_STAMP(4 * k + 4) }
       const int c0 = 8 * k;
       const int rk = (N - c0 + 31) >> 5;  // rows per lane follow the remaining height
       int* mv = mvl[k & 1];
       if (R >= 3 && rk == 3) fz = sq_panel<T, (R >= 3 ? 3 : 1)>(sbase, c0, lane, scr0, piv_all, mv, fz);
       else if (R >= 2 && rk == 2) fz = sq_panel<T, (R >= 2 ? 2 : 1)>(sbase, c0, lane, scr0, piv_all, mv, fz);
       else fz = sq_panel<T, 1>(sbase, c0, lane, scr0, piv_all, mv, fz);
+      if (tid == 0) { SQ_STAMP(4 * k + 5) }
       sq_sync(1, NTH);  // panel k and its pivots published
     }
     if (lane == 0) first_zero = fz;
@@ -367,6 +389,7 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
         if (NU > 1) sq_sync(3, 32 * NU);
         else __syncwarp();
         sq_tile_col<T>(sbase, c0, k + 1, uw, NU, ti, g, t);
+        if (uw == 0 && lane == 0) { SQ_STAMP(4 * k + 6) }
         sq_sync(2, NTH);  // block k+1 ready for the panel warp
         // the rest: inv(L11), then per column tile the interchanges (left tiles
         // too), the DMMA solve and the trailing update
@@ -379,6 +402,7 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
           sq_tile_solve<T>(sbase, c0, J, mbuf, lane, g, t);
           sq_tile_col<T>(sbase, c0, J, 0, 1, ti, g, t);
         }
+        if (uw == 0 && lane == 0) { SQ_STAMP(4 * k + 7) }
       } else {
         for (int J = uw; J < k; J += NU) sq_tile_moves<T>(sbase, J, mv, lane);
       }
@@ -390,9 +414,10 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
   __syncthreads();
   for (int j = tid; j < N; j += NTH) bulk_s2g(a + (long long)j * P.lda, sbase + 8u * (uint32_t)(j * S), 8u * N);
   bulk_commit();
-  for (int j = tid; j < N; j += NTH) P.ipiv[p * P.sp + j] = piv_all[j] + 1;
-  if (tid == 0) P.info[p] = first_zero;
+  for (int j = tid; j < N; j += NTH) P.ipiv[p * P.sp + j] = piv_all[j] + 1 + P.piv_offset;
+  if (tid == 0 && !(P.keep_info && P.info[p] != 0)) P.info[p] = first_zero ? first_zero + P.piv_offset : 0;
   bulk_wait_read0();
+  if (tid == 0) { SQ_STAMP(1) }
 }
 
 template <int T, int NU>
@@ -415,9 +440,9 @@ bool getrf_sq_ok(const double* a, long long stride, int lda, int m, int n) {
 }
 
 cudaError_t getrf_sq_launch(double* a, long long stride, int lda, int n, int* ipiv, long long sp, int* info,
-                            int batch, cudaStream_t s) {
+                            int piv_offset, int keep_info, int batch, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
-  GetrfSqArgs P{a, stride, lda, ipiv, sp, info};
+  GetrfSqArgs P{a, stride, lda, ipiv, sp, info, piv_offset, keep_info};
   // update warps per order (PBGPU_GETRF_SQ_NU = 1|2|3 overrides, tuning only)
   static const int nu_env = [] {
     const char* e = getenv("PBGPU_GETRF_SQ_NU");

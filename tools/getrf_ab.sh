@@ -1,5 +1,5 @@
 #!/bin/bash
-# getrf: new square kernel vs the previous dispatch (timing), then the LU tests
+# getrf: the square compile-time-shape kernel (getrf_sq.cu) vs the previous dispatch, then the LU tests
 mkdir -p gpurun_out
 {
 echo "== PBGPU_GETRF_SQ=0"; PBGPU_GETRF_SQ=0 timeout 200 python tools/quick_all.py getrf
