@@ -218,7 +218,7 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
   if (!legacy && getrf_reg_ok(L.m, L.n))
     return getrf_reg_launch(L.a, L.stride, L.lda, L.m, L.n, L.ipiv, L.stride_ipiv, L.info, L.batch, s);
   if (!legacy && getrf_sq_ok(L.a, L.stride, L.lda, L.m, L.n))
-    return getrf_sq_launch(L.a, L.stride, L.lda, L.n, L.ipiv, L.stride_ipiv, L.info, 0, 0, L.batch, s);
+    return getrf_sq_launch(L.a, L.stride, L.lda, L.n, L.ipiv, L.stride_ipiv, L.info, 0, 0, 0, L.batch, s);
   static const int blocked_from = [] {  // PBGPU_GETRF_BLOCKED_FROM=n: blocked path from this order on (tuning)
     const char* e = getenv("PBGPU_GETRF_BLOCKED_FROM");
     return e ? atoi(e) : 80;
@@ -245,15 +245,9 @@ cudaError_t getrf_launch(const GetrfLaunch& L, cudaStream_t s) {
     const int mm = L.m - j0;
     double* panel = L.a + (long long)j0 + (long long)j0 * L.lda;
     // the trailing square block, once it fits the shared-memory-resident kernel:
-    // factor it in one launch, then its interchanges on the columns left of it
-    if (j0 > 0 && L.m == L.n && !legacy && getrf_sq_ok(panel, L.stride, L.lda, mm, L.n - j0)) {
-      cudaError_t e = getrf_sq_launch(panel, L.stride, L.lda, mm, L.ipiv + j0, L.stride_ipiv, L.info, j0, 1,
-                                      L.batch, s);
-      if (e != cudaSuccess) return e;
-      dim3 grid(std::max(1, (j0 + 127) / 128), L.batch);
-      laswp_kernel<<<grid, 128, 0, s>>>(L.a, L.stride, L.lda, L.ipiv, L.stride_ipiv, j0, L.n, 0, j0);
-      return cudaGetLastError();
-    }
+    // one launch, its interchanges on the columns left of it fused in
+    if (j0 > 0 && L.m == L.n && !legacy && getrf_sq_ok(panel, L.stride, L.lda, mm, L.n - j0))
+      return getrf_sq_launch(panel, L.stride, L.lda, mm, L.ipiv + j0, L.stride_ipiv, L.info, j0, 1, j0, L.batch, s);
     // 1. factor the tall panel rows j0.., cols j0..j0+jb (pivots offset by j0)
     cudaError_t e = rows ? getrf_rows_launch(panel, L.stride, L.lda, mm, jb, L.ipiv + j0, L.stride_ipiv, L.info, j0,
                                              j0 > 0, L.batch, j0, L.n, s)

@@ -54,6 +54,7 @@ struct GetrfSqArgs {
   int* info;
   int piv_offset;  // added to the recorded pivots / failing column (trailing block of the blocked path)
   int keep_info;   // keep an info already set by an earlier panel
+  int left_cols;   // columns left of the block (same rows) that take its interchanges at the end
 };
 
 __host__ __device__ constexpr int sq_stride(int T) {  // = 4 mod 16 doubles: conflict-free DMMA fragments
@@ -80,7 +81,7 @@ __device__ __forceinline__ void sq_sync(int id, int count) {
 // and record the pivots.  Returns the updated first-zero column (1-based, 0 = none).
 template <int T, int RK>
 __device__ __forceinline__ int sq_panel(uint32_t sbase, int c0, int lane, uint32_t scr, int* piv_all, int* mv,
-                                        int fz) {
+                                        int* perm, int fz) {
   constexpr int N = 8 * T, S = sq_stride(T);
   double x[RK][8];
   int pos[RK];
@@ -178,6 +179,13 @@ __device__ __forceinline__ int sq_panel(uint32_t sbase, int c0, int lane, uint32
     base += __popc(m);
   }
   if (lane == 0) mv[0] = base;
+  if (perm) {  // warp-uniform: running row permutation (final position <- original row) for the left columns
+    __syncwarp();
+    const int e = lane < base ? mv[1 + lane] : 0;
+    const int src = lane < base ? perm[e & 0xffff] : 0;
+    __syncwarp();
+    if (lane < base) perm[e >> 16] = src;
+  }
   return fz;
 }
 
@@ -333,6 +341,7 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
   __shared__ int piv_all[N];                  // 0-based pivot row of every column
   __shared__ __align__(16) double scr[2][10];  // pivot row broadcast: 8 values, reciprocal, position
   __shared__ int mvl[2][20];                   // composed interchanges of block k (double-buffered)
+  __shared__ int perm_s[N];                    // left_cols > 0: final position <- original row of the block
   __shared__ __align__(16) double minv[64];    // inv(L11) of the current block
   __shared__ int first_zero;
   __shared__ __align__(8) uint64_t bar;
@@ -349,6 +358,8 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
     mbar_arrive_expect_tx(&bar, 8u * N * N);
     first_zero = 0;
   }
+  if (P.left_cols > 0)
+    for (int i = tid; i < N; i += NTH) perm_s[i] = i;
   __syncthreads();
   for (int j = tid; j < N; j += NTH) bulk_g2s(sm + j * S, a + (long long)j * P.lda, 8u * N, &bar);
   mbar_wait(&bar, 0);
@@ -364,9 +375,10 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
       const int c0 = 8 * k;
       const int rk = (N - c0 + 31) >> 5;  // rows per lane follow the remaining height
       int* mv = mvl[k & 1];
-      if (R >= 3 && rk == 3) fz = sq_panel<T, (R >= 3 ? 3 : 1)>(sbase, c0, lane, scr0, piv_all, mv, fz);
-      else if (R >= 2 && rk == 2) fz = sq_panel<T, (R >= 2 ? 2 : 1)>(sbase, c0, lane, scr0, piv_all, mv, fz);
-      else fz = sq_panel<T, 1>(sbase, c0, lane, scr0, piv_all, mv, fz);
+      int* perm = P.left_cols > 0 ? perm_s : nullptr;
+      if (R >= 3 && rk == 3) fz = sq_panel<T, (R >= 3 ? 3 : 1)>(sbase, c0, lane, scr0, piv_all, mv, perm, fz);
+      else if (R >= 2 && rk == 2) fz = sq_panel<T, (R >= 2 ? 2 : 1)>(sbase, c0, lane, scr0, piv_all, mv, perm, fz);
+      else fz = sq_panel<T, 1>(sbase, c0, lane, scr0, piv_all, mv, perm, fz);
       if (tid == 0) { SQ_STAMP(4 * k + 5) }
       sq_sync(1, NTH);  // panel k and its pivots published
     }
@@ -416,6 +428,37 @@ __global__ void __launch_bounds__(32 * (NU + 1), sq_min_blocks(T, NU)) getrf_sq_
   bulk_commit();
   for (int j = tid; j < N; j += NTH) P.ipiv[p * P.sp + j] = piv_all[j] + 1 + P.piv_offset;
   if (tid == 0 && !(P.keep_info && P.info[p] != 0)) P.info[p] = first_zero ? first_zero + P.piv_offset : 0;
+  // the block's interchanges on the columns left of it (the trailing block of the
+  // blocked path; LAPACK swaps whole rows, factor.hpp:175-183): every row moves
+  // from its original position to its final one, 16 columns per round, reads and
+  // writes separated by barriers (the moves form a permutation)
+  if (P.left_cols > 0) {
+    constexpr int RR = (N + NTH - 1) / NTH;  // rows per thread
+    constexpr int CW = RR > 1 ? 8 : 16;      // columns per round
+    int from[RR];
+    bool mvr[RR];
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+      const int r = tid + i * NTH;
+      from[i] = r < N ? perm_s[r] : 0;
+      mvr[i] = r < N && from[i] != r;
+    }
+    for (int q0 = -P.left_cols; q0 < 0; q0 += CW) {
+      double v[RR][CW];
+#pragma unroll
+      for (int i = 0; i < RR; ++i)
+#pragma unroll
+        for (int u = 0; u < CW; ++u)
+          v[i][u] = ldg_if(a + from[i] + (long long)(q0 + u) * P.lda, mvr[i] && q0 + u < 0, 0.0);
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < RR; ++i)
+#pragma unroll
+        for (int u = 0; u < CW; ++u)
+          stg_if(a + tid + i * NTH + (long long)(q0 + u) * P.lda, v[i][u], mvr[i] && q0 + u < 0);
+      __syncthreads();
+    }
+  }
   bulk_wait_read0();
   if (tid == 0) { SQ_STAMP(1) }
 }
@@ -440,9 +483,9 @@ bool getrf_sq_ok(const double* a, long long stride, int lda, int m, int n) {
 }
 
 cudaError_t getrf_sq_launch(double* a, long long stride, int lda, int n, int* ipiv, long long sp, int* info,
-                            int piv_offset, int keep_info, int batch, cudaStream_t s) {
+                            int piv_offset, int keep_info, int left_cols, int batch, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
-  GetrfSqArgs P{a, stride, lda, ipiv, sp, info, piv_offset, keep_info};
+  GetrfSqArgs P{a, stride, lda, ipiv, sp, info, piv_offset, keep_info, left_cols};
   // update warps per order (PBGPU_GETRF_SQ_NU = 1|2|3 overrides, tuning only)
   static const int nu_env = [] {
     const char* e = getenv("PBGPU_GETRF_SQ_NU");

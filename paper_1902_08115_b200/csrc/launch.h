@@ -123,9 +123,10 @@ cudaError_t getrf_cta_launch(double* a, long long stride, int lda, int m, int n,
 
 // square n = 40..96 (multiples of 8), compile-time shapes (getrf_sq.cu)
 bool getrf_sq_ok(const double* a, long long stride, int lda, int m, int n);
-// piv_offset / keep_info: the trailing square block of the blocked path
+// piv_offset / keep_info / left_cols: the trailing square block of the blocked path
+// (its interchanges are also applied to the left_cols columns left of it)
 cudaError_t getrf_sq_launch(double* a, long long stride, int lda, int n, int* ipiv, long long sp, int* info,
-                            int piv_offset, int keep_info, int batch, cudaStream_t s);
+                            int piv_offset, int keep_info, int left_cols, int batch, cudaStream_t s);
 
 // register-resident warp-per-problem LU, m, n <= 32 (getrf_reg.cu)
 bool getrf_reg_ok(int m, int n);

@@ -24,7 +24,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(a, a0, 8 * tot, cudaMemcpyDeviceToDevice);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    cudaError_t e = pbg::getrf_sq_launch(a, (long long)n * n, n, n, ipiv, n, info, batch, 0);
+    cudaError_t e = pbg::getrf_sq_launch(a, (long long)n * n, n, n, ipiv, n, info, 0, 0, 0, batch, 0);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     printf("rep %d: %.4f ms (%s / %s)\n", rep, ms, cudaGetErrorString(e), cudaGetErrorString(cudaGetLastError()));

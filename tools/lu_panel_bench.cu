@@ -22,7 +22,7 @@ __global__ void bench(long long* out, int reps, int c0) {
   int fz = 0;
   long long t0 = clock64();
   for (int i = 0; i < reps; ++i) {
-    fz = sq_panel<T, 1>(sbase, c0, lane, scr0, piv_all, mv, fz);
+    fz = sq_panel<T, 1>(sbase, c0, lane, scr0, piv_all, mv, nullptr, fz);
     __syncwarp();
   }
   long long t1 = clock64();
