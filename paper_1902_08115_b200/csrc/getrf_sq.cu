@@ -245,14 +245,13 @@ __device__ __forceinline__ void sq_tile_solve(uint32_t sbase, int c0, int J, uin
   const uint32_t bcol = sbase + 8u * (uint32_t)(c0 + t + (8 * J + g) * S);
   const double b0 = lds64(bcol), b1 = lds64(bcol + 32);
   const double m0 = lds64(mbuf + 8u * (uint32_t)(t * 8 + g)), m1 = lds64(mbuf + 8u * (uint32_t)((4 + t) * 8 + g));
+  // transposed product U^T = A12^T inv(L11)^T: the lane's results are rows 2t, 2t+1 of column g
   double d0 = 0.0, d1 = 0.0;
-  dmma(d0, d1, m0, b0);
-  dmma(d0, d1, m1, b1);
+  dmma(d0, d1, b0, m0);
+  dmma(d0, d1, b1, m1);
   const bool fin = fabs(d0) <= 1.7976931348623157e308 && fabs(d1) <= 1.7976931348623157e308;
   if (__all_sync(0xffffffffu, fin)) {
-    const uint32_t dcol = sbase + 8u * (uint32_t)(c0 + g + (8 * J + 2 * t) * S);
-    sts64(dcol, d0);
-    sts64(dcol + 8u * S, d1);
+    sts128(sbase + 8u * (uint32_t)(c0 + 2 * t + (8 * J + g) * S), d0, d1);
   } else if (lane < 8) {
     const uint32_t ub = sbase + 8u * (uint32_t)(c0 + (8 * J + lane) * S);
     const uint32_t lb = sbase + 8u * (uint32_t)(c0 + c0 * S);
@@ -290,40 +289,44 @@ __device__ __forceinline__ void sq_swap_solve(uint32_t sbase, int c0, const int*
   }
 }
 
-// One column tile J against row tiles I = i0, i0 + istep, .. < ti: C(I,J) -= L(I,k) U(k,J).
+// One column tile J against row tiles I = i0, i0 + istep, .. < ti: C(I,J) -= L(I,k) U(k,J),
+// computed as the transposed product C^T -= U^T L^T (the DMMA operands swap
+// roles), so a lane's two accumulators are rows 2t, 2t+1 of ONE column of the
+// tile: one 16-byte shared-memory access each way instead of two 8-byte ones
+// two columns apart (ncu: the C tiles were 39 % of the kernel's shared-memory
+// wavefronts, half of them bank conflicts of the column-pair pattern).
 template <int T>
 __device__ __forceinline__ void sq_tile_col(uint32_t sbase, int c0, int J, int i0, int istep, int ti, int g,
                                             int t) {
   constexpr int S = sq_stride(T);
   const uint32_t ucol = sbase + 8u * (uint32_t)(c0 + t + (8 * J + g) * S);
-  const double b0 = -lds64(ucol), b1 = -lds64(ucol + 32);
-  const uint32_t arow = sbase + 8u * (uint32_t)(c0 + 8 + g + (c0 + t) * S);        // L(I,k) fragments
-  const uint32_t crow = sbase + 8u * (uint32_t)(c0 + 8 + g + (8 * J + 2 * t) * S);  // C(I,J) accumulators
+  const double b0 = -lds64(ucol), b1 = -lds64(ucol + 32);                           // U(k,J)^T fragments (A operand)
+  const uint32_t arow = sbase + 8u * (uint32_t)(c0 + 8 + g + (c0 + t) * S);         // L(I,k)^T fragments (B operand)
+  const uint32_t crow = sbase + 8u * (uint32_t)(c0 + 8 + 2 * t + (8 * J + g) * S);  // C(I,J): rows 2t, 2t+1 of column g
   int I = i0;
   for (; I + istep < ti; I += 2 * istep) {  // two tiles in flight
     const uint32_t a = arow + 64u * (uint32_t)I, cc = crow + 64u * (uint32_t)I;
     const uint32_t a2 = a + 64u * (uint32_t)istep, cc2 = cc + 64u * (uint32_t)istep;
     const double a0 = lds64(a), a1 = lds64(a + 8u * (4 * S));
     const double e0 = lds64(a2), e1 = lds64(a2 + 8u * (4 * S));
-    double d0 = lds64(cc), d1 = lds64(cc + 8u * S);
-    double f0 = lds64(cc2), f1 = lds64(cc2 + 8u * S);
-    dmma(d0, d1, a0, b0);
-    dmma(f0, f1, e0, b0);
-    dmma(d0, d1, a1, b1);
-    dmma(f0, f1, e1, b1);
-    sts64(cc, d0);
-    sts64(cc + 8u * S, d1);
-    sts64(cc2, f0);
-    sts64(cc2 + 8u * S, f1);
+    double d0, d1, f0, f1;
+    lds128(cc, d0, d1);
+    lds128(cc2, f0, f1);
+    dmma(d0, d1, b0, a0);
+    dmma(f0, f1, b0, e0);
+    dmma(d0, d1, b1, a1);
+    dmma(f0, f1, b1, e1);
+    sts128(cc, d0, d1);
+    sts128(cc2, f0, f1);
   }
   if (I < ti) {
     const uint32_t a = arow + 64u * (uint32_t)I, cc = crow + 64u * (uint32_t)I;
     const double a0 = lds64(a), a1 = lds64(a + 8u * (4 * S));
-    double d0 = lds64(cc), d1 = lds64(cc + 8u * S);
-    dmma(d0, d1, a0, b0);
-    dmma(d0, d1, a1, b1);
-    sts64(cc, d0);
-    sts64(cc + 8u * S, d1);
+    double d0, d1;
+    lds128(cc, d0, d1);
+    dmma(d0, d1, b0, a0);
+    dmma(d0, d1, b1, a1);
+    sts128(cc, d0, d1);
   }
 }
 
