@@ -24,7 +24,11 @@ def apply_swaps(a, ipiv):
 
 
 @pytest.mark.parametrize("shape", [(24, 24), (48, 48), (96, 96), (192, 192), (13, 13), (9, 19), (19, 9),
-                                   (1, 1), (160, 160), (200, 150), (70, 250)])
+                                   (1, 1), (160, 160), (200, 150), (70, 250),
+                                   # getrf_sq: every order 40..96, and blocked paths whose trailing
+                                   # square block (72, 96, 40) runs on it with its left-column interchanges
+                                   (40, 40), (56, 56), (64, 64), (72, 72), (80, 80), (88, 88),
+                                   (104, 104), (128, 128), (136, 136)])
 def test_dgetrf_batched_vs_oracle(pb, orc, cuda, shape):
     import torch
     m, n = shape

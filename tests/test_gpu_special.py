@@ -6,7 +6,8 @@ pivot is an ordinary pivot, a +Inf pivot gives L_jj = Inf and a zero column belo
 dgetrf (factor.hpp:141-158): the strict ``>`` scan never picks a NaN candidate, a NaN
 diagonal keeps its row, an Inf candidate wins, and an exactly zero pivot records info
 without swapping.  Sizes cover potrf_reg (n <= 32), potrf_cta (33..160) and the blocked
-path (> 160); getrf_reg (<= 32), getrf_cta (< 80) and the blocked getrf_rows path.
+path (> 160); getrf_reg (<= 32), getrf_sq (square 40..96, also the trailing block of the
+blocked path: 104, 160, 192), getrf_cta (other shapes < 80) and the blocked getrf_rows path.
 """
 import numpy as np
 import pytest
@@ -111,7 +112,7 @@ def getrf_cases(rng, n):
     return cases
 
 
-@pytest.mark.parametrize("n", [3, 8, 24, 32, 48, 64, 79, 96, 130, 192])
+@pytest.mark.parametrize("n", [3, 8, 24, 32, 40, 48, 64, 79, 88, 96, 104, 130, 160, 192])
 def test_dgetrf_special_pivots(pb, orc, cuda, n):
     import torch
     rng = np.random.default_rng(1000 + n)

@@ -63,7 +63,7 @@ def potrf():
 
 
 def getrf():
-    for n in (8, 24, 32, 48, 79, 96, 130):
+    for n in (8, 24, 32, 40, 48, 64, 79, 96, 104, 130, 160):  # 40..96 and the 104/160 tails: getrf_sq
         A = rand(3, n, n)
         ip = torch.empty((3, n), dtype=torch.int32, device=dev)
         info = torch.empty(3, dtype=torch.int32, device=dev)
