@@ -368,7 +368,8 @@ def series_dgemm(S: Series):
     import torch
     pb, dev, stream = S.pb, S.dev, S.stream
     out = {}
-    for n, batch in ((32, 65536), (64, 16384), (128, 4096), (256, 1024)):
+    # 8 and 16: the small-n branch of the size switch (gemm_cmsmall.cu, a warp per problem)
+    for n, batch in ((8, 1048576), (16, 262144), (32, 65536), (64, 16384), (128, 4096), (256, 1024)):
         g = torch.Generator(device=dev).manual_seed(n)
         A = torch.rand((batch, n, n), generator=g, device=dev, dtype=torch.float64) * 2 - 1
         B = torch.rand((batch, n, n), generator=g, device=dev, dtype=torch.float64) * 2 - 1

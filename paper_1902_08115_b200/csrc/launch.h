@@ -66,6 +66,12 @@ bool gemm_cm_ok(int s, const double* a, const double* b, const double* c, long l
                 long long sc, int lda, int ldb, int ldc);
 cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b, double beta, double* c,
                            long long batch, cudaStream_t st);
+// column-major small problems, m, n <= 32, any k / trans / leading dimensions: warp per problem
+// (gemm_cmsmall.cu) — the small-n branch of the size switch (variant D, gemm.hpp:190-204)
+bool gemm_cmsmall_ok(int m, int n);
+cudaError_t gemm_cmsmall_launch(int ta, int tb, int m, int n, int k, double alpha, const double* a, int lda,
+                                long long sa, const double* b, int ldb, long long sb, double beta, double* c,
+                                int ldc, long long sc, long long batch, cudaStream_t s);
 
 }  // namespace pbg
 

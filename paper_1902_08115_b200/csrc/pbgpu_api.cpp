@@ -375,6 +375,10 @@ static int dgemm_impl(const char* routine, bool batched, char transa, char trans
                          if (ta == 0 && tb == 0 && m == n && n == k &&
                              gemm_cm_ok(m, (const double*)p[0], (const double*)p[1], o.c, sa, sb, sc, lda, ldb, ldc))
                            return gemm_cm_launch(m, alpha, (const double*)p[0], (const double*)p[1], beta, o.d, nb, s);
+                         // small-n branch (variant D's role): a warp per problem, no 64x64 tile padding
+                         if (gemm_cmsmall_ok(m, n))
+                           return gemm_cmsmall_launch(ta != 0, tb != 0, m, n, k, alpha, (const double*)p[0], lda, sa,
+                                                      (const double*)p[1], ldb, sb, beta, o.d, ldc, sc, nb, s);
                          GemmLaunch g;
                          // M side: op(A)(i, l); N side: op(B)(l, j) as (x = j, l).
                          g.lay_a = ta == 0 ? L_MNC : L_KC;

@@ -39,6 +39,39 @@ def test_dgemm_batched_device(pb, orc, cuda, ta, tb, shape):
         assert rel_frob(got[p].T, want) <= tol(k)
 
 
+@pytest.mark.parametrize("ta,tb", [("n", "n"), ("n", "t"), ("t", "n"), ("t", "t")])
+@pytest.mark.parametrize("shape", [(4, 4, 4), (8, 8, 8), (16, 16, 16), (24, 24, 24), (32, 32, 32), (5, 31, 3),
+                                   (32, 7, 70), (17, 25, 33), (8, 16, 200), (1, 32, 1)])
+def test_dgemm_small_cm(pb, orc, cuda, ta, tb, shape):
+    """The small-n branch (gemm_cmsmall.cu: m, n <= 32, warp per problem): every trans pair, ragged
+    shapes, k over several 32-chunks, padded and odd leading dimensions, beta = 0 with NaN in C."""
+    import torch
+    m, n, k = shape
+    rng = np.random.default_rng(hash((ta, tb, shape, "small")) % 2**32)
+    batch = 37
+    ar, ac = (m, k) if ta == "n" else (k, m)
+    br, bc = (k, n) if tb == "n" else (n, k)
+    for (pa, pb_, pc, alpha, beta) in [(0, 0, 0, 1.0, 1.0), (3, 1, 5, -0.75, 0.0), (2, 4, 2, 1.5, -0.5)]:
+        lda, ldb, ldc = ar + pa, br + pb_, m + pc
+        A = rng.uniform(-1, 1, (batch, ac, lda))
+        B = rng.uniform(-1, 1, (batch, bc, ldb))
+        Cm = rng.uniform(-1, 1, (batch, n, ldc))
+        if beta == 0.0:
+            Cm[:, :, :m] = np.nan  # never read
+        dA, dB, dC = (torch.from_numpy(x.copy()).to(cuda) for x in (A, B, Cm))
+        r = pb.dgemm_batched(ta, tb, m, n, k, alpha, dA, lda, lda * ac, dB, ldb, ldb * bc, beta, dC, ldc, ldc * n, batch)
+        assert r.info == 0 and r.flops == 2 * m * n * k * batch
+        got = dC.cpu().numpy()
+        for p in range(batch):
+            want = F(Cm[p].T)
+            a = F(A[p].T)
+            b = F(B[p].T)
+            orc.dgemm(ch(ta), ch(tb), m, n, k, alpha, ptr(a), lda, ptr(b), ldb, beta, ptr(want), ldc)
+            assert not np.isnan(got[p].T[:m]).any()
+            assert rel_frob(got[p].T[:m], want[:m]) <= tol(k)
+            assert same_bits(got[p].T[m:], F(Cm[p].T)[m:])  # pad rows of C untouched
+
+
 def test_dgemm_cfg1_full_batch(pb, orc, cuda):
     """Config 1 at full size: 16384 problems of 64^3, alpha = beta = 1; every problem checked."""
     import torch
