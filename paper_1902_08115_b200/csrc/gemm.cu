@@ -296,9 +296,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
       for (int h = 0; h < WH; ++h) {
         const int i = tm * TM + ib + h * 8 + 2 * t, j = tn * TN + jb + f * 8 + g;
         dst[f][h][0] = dst[f][h][1] = 0.0;
-        // entries outside the uplo triangle are never stored: do not read them either
-        const bool tri = P.uplo == 0 || (P.uplo == 1 ? i + 1 >= j : i <= j);
-        if (j < P.n && live && tri) {
+        if (j < P.n && live) {
           const double* cp = cbase + out_off<OUT_PM>(P.o.ldc, i, j);
           if (P.o.vec && i + 1 < P.m) {
             double2 v = *reinterpret_cast<const double2*>(cp);
@@ -333,46 +331,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
     for (int f = 0; f < WF; ++f)
 #pragma unroll
       for (int h = 0; h < WH; ++h) acc[f][h][0] = acc[f][h][1] = 0.0;
-    // 8x8 tiles of this warp that hold any stored entry: inside m x n and, for
-    // syrk-style outputs, touching the uplo triangle.  Edge and diagonal CTA
-    // tiles skip the rest (ragged orders put most of an edge tile out of range).
-    unsigned live_tiles = 0;
-#pragma unroll
-    for (int f = 0; f < WF; ++f)
-#pragma unroll
-      for (int h = 0; h < WH; ++h) {
-        const int ti0 = i0 + ib + h * 8, tj0 = j0 + jb + f * 8;
-        bool on = ti0 < P.m && tj0 < P.n;
-        if (P.uplo == 1) on = on && ti0 + 7 >= tj0;
-        if (P.uplo == 2) on = on && ti0 <= tj0 + 7;
-        live_tiles |= (on ? 1u : 0u) << (f * WH + h);
-      }
-    constexpr unsigned ALL_TILES = (1u << (WF * WH)) - 1u;
 
     for (int kc = 0; kc < P.nk; ++kc) {
       const int kvalid = min(BK, P.k - kc * BK);
       mbar_wait(&full[stage], phase);
       const double* sA = smem + (size_t)stage * STAGE;
       const double* sB = sA + TA::SIZE;
-      if (live_tiles == 0u) {
-        // nothing of this warp's region is stored: release the stage
-      } else if (live_tiles != ALL_TILES) {
-        const int ksteps = (kvalid + 3) >> 2;
-        for (int ks = 0; ks < ksteps; ++ks) {
-          const int l = ks * 4 + t;
-          const bool in = l < kvalid;
-          double av[WF], bv[WH];
-#pragma unroll
-          for (int f = 0; f < WF; ++f) av[f] = in ? sB[TB::at(jb + f * 8 + g, l)] : 0.0;
-#pragma unroll
-          for (int h = 0; h < WH; ++h) bv[h] = in ? sA[TA::at(ib + h * 8 + g, l)] : 0.0;
-#pragma unroll
-          for (int f = 0; f < WF; ++f)
-#pragma unroll
-            for (int h = 0; h < WH; ++h)
-              if ((live_tiles >> (f * WH + h)) & 1u) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
-        }
-      } else if (kvalid == BK) {
+      if (kvalid == BK) {
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
           const int l = ks * 4 + t;
