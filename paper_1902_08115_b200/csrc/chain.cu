@@ -128,10 +128,46 @@ static int chain_engine_from() {
   return v;
 }
 
-cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
+// The order classes are independent problems: they are issued round-robin on a
+// few side streams (forked from / joined to the caller's stream with events), so
+// the tail of one class's launches overlaps the next class's instead of draining
+// the GPU ~250 times per call.  PBGPU_CHAIN_STREAMS = 1 keeps one stream (A/B).
+constexpr int kChainStreams = 4;
+struct ChainPool {
+  cudaStream_t st[kChainStreams] = {};
+  cudaEvent_t done[kChainStreams] = {};
+  cudaEvent_t fork = nullptr;
+  bool ready = false;
+};
+static ChainPool* chain_pool() {
+  static thread_local ChainPool pools[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  ChainPool& P = pools[dev];
+  if (!P.ready) {
+    for (int i = 0; i < kChainStreams; ++i) {
+      if (cudaStreamCreateWithFlags(&P.st[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+      if (cudaEventCreateWithFlags(&P.done[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    if (cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    P.ready = true;
+  }
+  return &P;
+}
+static int chain_streams() {
+  static const int v = [] {
+    const char* e = getenv("PBGPU_CHAIN_STREAMS");
+    const int n = e ? atoi(e) : kChainStreams;
+    return n < 1 ? 1 : (n > kChainStreams ? kChainStreams : n);
+  }();
+  return v;
+}
+
+cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
   if (L.batch <= 0) return cudaSuccess;
   mempool_keep();
   cudaError_t e;
+  cudaStream_t s = s0;  // the stream of the current class (a side stream after the fork)
   // The split by order is planned on the host: from the caller's host copies of
   // n / offset when given (no synchronisation), else from a device -> host copy.
   std::vector<int> nv(L.batch);
@@ -158,6 +194,33 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       big[nv[p]].push_back(p);
     }
   }
+  ChainPool* pool = chain_streams() > 1 ? chain_pool() : nullptr;
+  const int nstreams = pool ? chain_streams() : 1;
+  int next_stream = 0;
+  bool forked = false;
+  auto fork = [&]() -> cudaError_t {  // side streams start after everything queued on s0 so far
+    if (!pool || forked) return cudaSuccess;
+    cudaError_t fe = cudaEventRecord(pool->fork, s0);
+    for (int i = 0; i < nstreams && fe == cudaSuccess; ++i) fe = cudaStreamWaitEvent(pool->st[i], pool->fork, 0);
+    forked = fe == cudaSuccess;
+    return fe;
+  };
+  auto class_stream = [&]() -> cudaStream_t {
+    if (!pool) return s0;
+    cudaStream_t cs = pool->st[next_stream];
+    next_stream = (next_stream + 1) % nstreams;
+    return cs;
+  };
+  auto join = [&]() -> cudaError_t {  // s0 continues after every side stream
+    if (!pool || !forked) return cudaSuccess;
+    cudaError_t je = cudaSuccess;
+    for (int i = 0; i < nstreams && je == cudaSuccess; ++i) {
+      je = cudaEventRecord(pool->done[i], pool->st[i]);
+      if (je == cudaSuccess) je = cudaStreamWaitEvent(s0, pool->done[i], 0);
+    }
+    forked = false;
+    return je;
+  };
   // Small orders: sorted by order and launched per 8-column class, so every
   // launch is sized (shared memory, warps, unrolling) for its own problems.
   std::sort(small.begin(), small.end(), [&](int x, int y) { return nv[x] < nv[y]; });
@@ -179,7 +242,9 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
     cudaMemcpyAsync(d_idx, small.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_n, sn.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_off, so.data(), sizeof(long long) * nsm, cudaMemcpyHostToDevice, s);
+    if ((e = fork()) != cudaSuccess) return e;
     for (size_t b0 = 0; b0 < nsm && e == cudaSuccess;) {
+      s = class_stream();
       const int cls = (sn[b0] + 7) / 8;
       size_t b1 = b0;
       while (b1 < nsm && (sn[b1] + 7) / 8 == cls) ++b1;
@@ -235,6 +300,8 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
       }
       b0 = b1;
     }
+    s = s0;
+    if (e == cudaSuccess) e = join();
     if (e == cudaSuccess) {
       scatter_info_kernel<<<std::max(1, (int)((nsm + 255) / 256)), 256, 0, s>>>(d_info, d_idx, L.info, (int)nsm);
       e = cudaGetLastError();
@@ -248,7 +315,10 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
   // large orders, per distinct n: the syrk, the blocked Cholesky and the solve
   // run straight on the caller's buffers through per-problem offsets (the
   // class's members), so nothing is gathered or scattered
-  for (auto& kv : big) {
+  if (!big.empty() && (e = fork()) != cudaSuccess) return e;
+  for (auto it = big.rbegin(); it != big.rend(); ++it) {  // largest orders first
+    auto& kv = *it;
+    s = class_stream();
     const int n = kv.first, cnt = (int)kv.second.size();
     int *d_i = nullptr, *w_info = nullptr;
     long long* d_o = nullptr;
@@ -329,7 +399,8 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s) {
     cudaFreeAsync(w_info, s);
     if (e != cudaSuccess) return e;
   }
-  return cudaSuccess;
+  s = s0;
+  return join();
 }
 
 }  // namespace pbg
