@@ -225,11 +225,11 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
   // launch is sized (shared memory, warps, unrolling) for its own problems.
   std::sort(small.begin(), small.end(), [&](int x, int y) { return nv[x] < nv[y]; });
   const size_t nsm = small.size();
+  int *d_idx = nullptr, *d_n = nullptr, *d_info = nullptr;
+  long long* d_off = nullptr;
+  std::vector<long long> so(nsm);
+  std::vector<int> sn(nsm);
   if (nsm) {
-    int *d_idx = nullptr, *d_n = nullptr, *d_info = nullptr;
-    long long* d_off = nullptr;
-    std::vector<long long> so(nsm);
-    std::vector<int> sn(nsm);
     for (size_t q = 0; q < nsm; ++q) {
       so[q] = ov[small[q]];
       sn[q] = nv[small[q]];
@@ -242,7 +242,109 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
     cudaMemcpyAsync(d_idx, small.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_n, sn.data(), sizeof(int) * nsm, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(d_off, so.data(), sizeof(long long) * nsm, cudaMemcpyHostToDevice, s);
-    if ((e = fork()) != cudaSuccess) return e;
+  }
+  // column-major large orders factor in a strided workspace (A gathered, S = C + A A^T,
+  // then L): one per side stream, sized for the largest class that stream will see and
+  // allocated here on the caller's stream — large stream-ordered allocations issued
+  // concurrently from several streams made the pool serialise or grow (cm 32 -> 49 ms)
+  double* ws_stream[kChainStreams] = {};
+  if (!L.pm && !big.empty()) {
+    size_t need[kChainStreams] = {};
+    int k = 0;
+    for (auto it = big.rbegin(); it != big.rend(); ++it, k = (k + 1) % nstreams)
+      need[k] = std::max(need[k], (size_t)2 * it->first * it->first * it->second.size());
+    for (int i = 0; i < nstreams; ++i)
+      if (need[i] && (e = cudaMallocAsync(&ws_stream[i], sizeof(double) * need[i], s0)) != cudaSuccess) return e;
+  }
+  if ((e = fork()) != cudaSuccess) return e;
+  // large orders, per distinct n: the syrk, the blocked Cholesky and the solve
+  // run straight on the caller's buffers through per-problem offsets (the
+  // class's members), so nothing is gathered or scattered
+  for (auto it = big.rbegin(); it != big.rend(); ++it) {  // largest orders first
+    auto& kv = *it;
+    const int stream_slot = next_stream;
+    s = class_stream();
+    const int n = kv.first, cnt = (int)kv.second.size();
+    int *d_i = nullptr, *w_info = nullptr;
+    long long* d_o = nullptr;
+    if ((e = cudaMallocAsync(&d_i, sizeof(int) * cnt, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&w_info, sizeof(int) * cnt, s)) != cudaSuccess ||
+        (e = cudaMallocAsync(&d_o, sizeof(long long) * cnt, s)) != cudaSuccess)
+      return e;
+    std::vector<long long> ob(cnt);
+    bool even = true;
+    for (int q = 0; q < cnt; ++q) {
+      ob[q] = ov[kv.second[q]];
+      even = even && (ob[q] % 2 == 0);
+    }
+    cudaMemcpyAsync(d_i, kv.second.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(d_o, ob.data(), sizeof(long long) * cnt, cudaMemcpyHostToDevice, s);
+    double* wc = nullptr;  // column-major: the factor's workspace (S = C + A A^T, then L)
+    double* wa = nullptr;
+    if (!L.pm) {
+      // column-major: the engine's tensor-map path needs strided operands (its
+      // per-column bulk copies measured 1.7x slower here), so A is gathered once,
+      // S = C + A A^T lands in a strided workspace (C read through the offsets),
+      // is factored there, and only L's lower triangle goes back to C
+      const long long nn = (long long)n * n;
+      wa = ws_stream[pool ? stream_slot : 0];
+      wc = wa + nn * cnt;
+      gather_kernel<<<grid2(nn, cnt), 256, 0, s>>>(L.A, d_o, wa, n);
+      GemmLaunch g;  // dsyrk('l','n'): S = C + A A^T
+      g.lay_a = g.lay_b = L_MNC;
+      g.a.base = g.b.base = wa; g.a.stride = g.b.stride = nn; g.a.ld = g.b.ld = n; g.a.bulk = g.b.bulk = 1;
+      g.o.c = L.C; g.o.offs_c = d_o; g.o.d = wc; g.o.sd = nn; g.o.ldc = g.o.ldd = n;
+      g.o.vec = even && n % 2 == 0 && (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
+      g.m = g.n = g.k = n;
+      g.alpha = 1.0; g.beta = 1.0; g.uplo = 1; g.batch = cnt;
+      e = gemm_launch(g, s);
+      if (e == cudaSuccess) {
+        PotrfLaunch P;
+        P.a = wc; P.stride = nn; P.lda = n; P.n = n; P.info = w_info; P.batch = cnt;
+        e = potrf_launch(P, s);
+      }
+    } else {
+      SyrkPotrfLaunch S;
+      S.a = S.b = L.A; S.c = L.C; S.d = L.C;
+      S.offs = d_o;
+      S.offs_even = even && (reinterpret_cast<uintptr_t>(L.A) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
+      S.cna = S.cnb = S.cnc = S.cnd = n;
+      S.n = S.k = n;
+      S.info = w_info;
+      S.batch = cnt;
+      e = syrk_potrf_launch(S, s);
+    }
+    if (e == cudaSuccess) {
+      TrsmLaunch T;
+      T.pm = L.pm;
+      T.lower = 1; T.trans = 1; T.unit = 0;
+      T.mm = T.nn = n;
+      T.alpha = 1.0;
+      T.a = L.pm ? L.C : wc; T.offs_a = L.pm ? d_o : nullptr; T.sa = (long long)n * n; T.lda = n;
+      T.b = L.B; T.ldb = n;
+      T.d = L.B; T.ldd = n;
+      T.offs_b = d_o;
+      T.info = w_info;
+      T.skip_nonzero = 1;
+      T.batch = cnt;
+      e = trsm_launch(T, s);
+    }
+    if (e == cudaSuccess && !L.pm) {
+      scatter_lower_kernel<<<grid2((long long)n * n, cnt), 256, 0, s>>>(wc, L.C, d_o, n);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      scatter_info_kernel<<<std::max(1, (cnt + 255) / 256), 256, 0, s>>>(w_info, d_i, L.info, cnt);
+      e = cudaGetLastError();
+    }
+    cudaFreeAsync(d_i, s);
+    cudaFreeAsync(d_o, s);
+    cudaFreeAsync(w_info, s);
+    if (e != cudaSuccess) return e;
+  }
+  // small orders after the large ones (the longest work first), on the same side streams
+  if (nsm) {
     for (size_t b0 = 0; b0 < nsm && e == cudaSuccess;) {
       s = class_stream();
       const int cls = (sn[b0] + 7) / 8;
@@ -300,8 +402,13 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
       }
       b0 = b1;
     }
-    s = s0;
-    if (e == cudaSuccess) e = join();
+  }
+  if (e != cudaSuccess) return e;
+  s = s0;
+  if ((e = join()) != cudaSuccess) return e;
+  for (int i = 0; i < kChainStreams; ++i)
+    if (ws_stream[i]) cudaFreeAsync(ws_stream[i], s0);
+  if (nsm) {
     if (e == cudaSuccess) {
       scatter_info_kernel<<<std::max(1, (int)((nsm + 255) / 256)), 256, 0, s>>>(d_info, d_idx, L.info, (int)nsm);
       e = cudaGetLastError();
@@ -312,95 +419,7 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
     cudaFreeAsync(d_off, s);
     if (e != cudaSuccess) return e;
   }
-  // large orders, per distinct n: the syrk, the blocked Cholesky and the solve
-  // run straight on the caller's buffers through per-problem offsets (the
-  // class's members), so nothing is gathered or scattered
-  if (!big.empty() && (e = fork()) != cudaSuccess) return e;
-  for (auto it = big.rbegin(); it != big.rend(); ++it) {  // largest orders first
-    auto& kv = *it;
-    s = class_stream();
-    const int n = kv.first, cnt = (int)kv.second.size();
-    int *d_i = nullptr, *w_info = nullptr;
-    long long* d_o = nullptr;
-    if ((e = cudaMallocAsync(&d_i, sizeof(int) * cnt, s)) != cudaSuccess ||
-        (e = cudaMallocAsync(&w_info, sizeof(int) * cnt, s)) != cudaSuccess ||
-        (e = cudaMallocAsync(&d_o, sizeof(long long) * cnt, s)) != cudaSuccess)
-      return e;
-    std::vector<long long> ob(cnt);
-    bool even = true;
-    for (int q = 0; q < cnt; ++q) {
-      ob[q] = ov[kv.second[q]];
-      even = even && (ob[q] % 2 == 0);
-    }
-    cudaMemcpyAsync(d_i, kv.second.data(), sizeof(int) * cnt, cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(d_o, ob.data(), sizeof(long long) * cnt, cudaMemcpyHostToDevice, s);
-    double* wc = nullptr;  // column-major: the factor's workspace (S = C + A A^T, then L)
-    double* wa = nullptr;
-    if (!L.pm) {
-      // column-major: the engine's tensor-map path needs strided operands (its
-      // per-column bulk copies measured 1.7x slower here), so A is gathered once,
-      // S = C + A A^T lands in a strided workspace (C read through the offsets),
-      // is factored there, and only L's lower triangle goes back to C
-      const long long nn = (long long)n * n;
-      if ((e = cudaMallocAsync(&wa, sizeof(double) * nn * cnt * 2, s)) != cudaSuccess) return e;
-      wc = wa + nn * cnt;
-      gather_kernel<<<grid2(nn, cnt), 256, 0, s>>>(L.A, d_o, wa, n);
-      GemmLaunch g;  // dsyrk('l','n'): S = C + A A^T
-      g.lay_a = g.lay_b = L_MNC;
-      g.a.base = g.b.base = wa; g.a.stride = g.b.stride = nn; g.a.ld = g.b.ld = n; g.a.bulk = g.b.bulk = 1;
-      g.o.c = L.C; g.o.offs_c = d_o; g.o.d = wc; g.o.sd = nn; g.o.ldc = g.o.ldd = n;
-      g.o.vec = even && n % 2 == 0 && (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
-      g.m = g.n = g.k = n;
-      g.alpha = 1.0; g.beta = 1.0; g.uplo = 1; g.batch = cnt;
-      e = gemm_launch(g, s);
-      if (e == cudaSuccess) {
-        PotrfLaunch P;
-        P.a = wc; P.stride = nn; P.lda = n; P.n = n; P.info = w_info; P.batch = cnt;
-        e = potrf_launch(P, s);
-      }
-    } else {
-      SyrkPotrfLaunch S;
-      S.a = S.b = L.A; S.c = L.C; S.d = L.C;
-      S.offs = d_o;
-      S.offs_even = even && (reinterpret_cast<uintptr_t>(L.A) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
-      S.cna = S.cnb = S.cnc = S.cnd = n;
-      S.n = S.k = n;
-      S.info = w_info;
-      S.batch = cnt;
-      e = syrk_potrf_launch(S, s);
-    }
-    if (e == cudaSuccess) {
-      TrsmLaunch T;
-      T.pm = L.pm;
-      T.lower = 1; T.trans = 1; T.unit = 0;
-      T.mm = T.nn = n;
-      T.alpha = 1.0;
-      T.a = L.pm ? L.C : wc; T.offs_a = L.pm ? d_o : nullptr; T.sa = (long long)n * n; T.lda = n;
-      T.b = L.B; T.ldb = n;
-      T.d = L.B; T.ldd = n;
-      T.offs_b = d_o;
-      T.info = w_info;
-      T.skip_nonzero = 1;
-      T.batch = cnt;
-      e = trsm_launch(T, s);
-    }
-    if (e == cudaSuccess && !L.pm) {
-      scatter_lower_kernel<<<grid2((long long)n * n, cnt), 256, 0, s>>>(wc, L.C, d_o, n);
-      e = cudaGetLastError();
-    }
-    if (e == cudaSuccess) {
-      scatter_info_kernel<<<std::max(1, (cnt + 255) / 256), 256, 0, s>>>(w_info, d_i, L.info, cnt);
-      e = cudaGetLastError();
-    }
-    if (wa) cudaFreeAsync(wa, s);
-    cudaFreeAsync(d_i, s);
-    cudaFreeAsync(d_o, s);
-    cudaFreeAsync(w_info, s);
-    if (e != cudaSuccess) return e;
-  }
-  s = s0;
-  return join();
+  return cudaSuccess;
 }
 
 }  // namespace pbg
