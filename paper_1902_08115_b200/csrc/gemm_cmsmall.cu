@@ -42,8 +42,9 @@ struct CmSmallArgs {
 
 constexpr int kCmsWarps = 4;
 
+// registers capped so that shared memory, not the register file, bounds residency (3 CTAs at MT = 4)
 template <int MT>
-__global__ void __launch_bounds__(32 * kCmsWarps) gemm_cmsmall_kernel(const __grid_constant__ CmSmallArgs P) {
+__global__ void __launch_bounds__(32 * kCmsWarps, MT >= 3 ? 3 : (MT == 2 ? 5 : 9)) gemm_cmsmall_kernel(const __grid_constant__ CmSmallArgs P) {
   constexpr int MR = 8 * MT;      // rows / columns covered (m, n <= MR)
   constexpr int SA = MR + 4;      // As[l][i]: stride between k-rows
   constexpr int SB = 36;          // Bs[j][l]: stride between columns of op(B)
@@ -124,6 +125,26 @@ __global__ void __launch_bounds__(32 * kCmsWarps) gemm_cmsmall_kernel(const __gr
       }
     }
     // ---- epilogue: d = alpha * acc + beta * c on the valid part ----
+    // every C load first, then the stores: a store to C between two loads would pin
+    // the loads in program order (they may alias) and serialise MT*MT DRAM round trips
+    double cv[MT][MT][2];
+#pragma unroll
+    for (int J = 0; J < MT; ++J)
+#pragma unroll
+      for (int I = 0; I < MT; ++I) {
+        const int i = 8 * I + 2 * t, j = 8 * J + g;
+        cv[J][I][0] = cv[J][I][1] = 0.0;
+        if (!use_c || j >= n || i >= m) continue;
+        const double* cp = c + i + (long long)j * P.ldc;
+        if (P.vec && i + 1 < m) {
+          const double2 v = *reinterpret_cast<const double2*>(cp);
+          cv[J][I][0] = v.x;
+          cv[J][I][1] = v.y;
+        } else {
+          cv[J][I][0] = cp[0];
+          if (i + 1 < m) cv[J][I][1] = cp[1];
+        }
+      }
 #pragma unroll
     for (int J = 0; J < MT; ++J)
 #pragma unroll
@@ -132,19 +153,11 @@ __global__ void __launch_bounds__(32 * kCmsWarps) gemm_cmsmall_kernel(const __gr
         if (j >= n || i >= m) continue;
         double* cp = c + i + (long long)j * P.ldc;
         const bool two = i + 1 < m;
-        double r0 = acc[J][I][0] * P.alpha, r1 = acc[J][I][1] * P.alpha;
+        const double r0 = use_c ? fma(P.alpha, acc[J][I][0], P.beta * cv[J][I][0]) : acc[J][I][0] * P.alpha;
+        const double r1 = use_c ? fma(P.alpha, acc[J][I][1], P.beta * cv[J][I][1]) : acc[J][I][1] * P.alpha;
         if (P.vec && two) {
-          if (use_c) {
-            const double2 cv = *reinterpret_cast<const double2*>(cp);
-            r0 = fma(P.alpha, acc[J][I][0], P.beta * cv.x);
-            r1 = fma(P.alpha, acc[J][I][1], P.beta * cv.y);
-          }
           *reinterpret_cast<double2*>(cp) = make_double2(r0, r1);
         } else {
-          if (use_c) {
-            r0 = fma(P.alpha, acc[J][I][0], P.beta * cp[0]);
-            if (two) r1 = fma(P.alpha, acc[J][I][1], P.beta * cp[1]);
-          }
           cp[0] = r0;
           if (two) cp[1] = r1;
         }
