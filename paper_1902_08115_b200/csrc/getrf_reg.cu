@@ -40,8 +40,11 @@ struct GetrfRegArgs {
 constexpr int kLuRegWarps = 4;
 
 // LD != 0: compile-time leading dimension (packed square problems, lda == m == n == N)
+#ifndef PB_LUREG_MINB
+#define PB_LUREG_MINB 6
+#endif
 template <int N, int LD>
-__global__ void __launch_bounds__(32 * kLuRegWarps, 4) getrf_reg_kernel(const __grid_constant__ GetrfRegArgs P) {
+__global__ void __launch_bounds__(32 * kLuRegWarps, N <= 24 ? PB_LUREG_MINB : 4) getrf_reg_kernel(const __grid_constant__ GetrfRegArgs P) {
   __shared__ __align__(16) double rowbuf[kLuRegWarps][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long p = (long long)blockIdx.x * kLuRegWarps + warp;
@@ -79,10 +82,7 @@ __global__ void __launch_bounds__(32 * kLuRegWarps, 4) getrf_reg_kernel(const __
       for (int j = c & ~1; j < N; j += 2) sts128(buf + 8u * j, x[j], x[j + 1]);
     }
     __syncwarp();
-    double u[N];
-#pragma unroll
-    for (int j = c & ~1; j < N; j += 2) lds128(buf + 8u * j, u[j], u[j + 1]);
-    const double pv = u[c];
+    const double pv = lds64(buf + 8u * c);
     const bool nz = pv != 0.0;
     if (lane == c) my_ipiv = q + 1;
     if (!nz && first_zero == 0) first_zero = c + 1;
@@ -99,9 +99,17 @@ __global__ void __launch_bounds__(32 * kLuRegWarps, 4) getrf_reg_kernel(const __
       // zero multipliers skip only the rest of the reference's nr = 4 column
       // block (factor.hpp:160-165); later blocks take the plain trailing
       // update (207-215), where 0 * Inf = NaN
+      // pivot row pairs loaded next to their use (volatile loads stay in place):
+      // the live set is the row plus one pair, not two rows
+      const bool fz = f == 0.0;
 #pragma unroll
-      for (int j = c + 1; j < N; ++j)
-        if (f != 0.0 || j > (c | 3)) x[j] = fma(-f, u[j], x[j]);
+      for (int j = (c + 1) & ~1; j < N; j += 2) {
+        if (fz && j + 1 <= (c | 3)) continue;
+        double u0, u1;
+        lds128(buf + 8u * j, u0, u1);
+        if (j >= c + 1 && !(fz && j <= (c | 3))) x[j] = fma(-f, u0, x[j]);
+        x[j + 1] = fma(-f, u1, x[j + 1]);
+      }
     }
   }
 #pragma unroll
