@@ -41,7 +41,7 @@ constexpr int kLuRegWarps = 4;
 
 // LD != 0: compile-time leading dimension (packed square problems, lda == m == n == N)
 #ifndef PB_LUREG_MINB
-#define PB_LUREG_MINB 6
+#define PB_LUREG_MINB 7
 #endif
 template <int N, int LD>
 __global__ void __launch_bounds__(32 * kLuRegWarps, N <= 24 ? PB_LUREG_MINB : 4) getrf_reg_kernel(const __grid_constant__ GetrfRegArgs P) {
