@@ -37,7 +37,8 @@ struct CmSmallArgs {
   int m, n, k, ta, tb;
   double alpha, beta;
   long long batch;
-  int vec;  // 16-byte C accesses allowed
+  int vec;   // 16-byte C accesses allowed
+  int uplo;  // 0 full, 1 lower (i >= j), 2 upper (i <= j): entries outside are neither read nor written (dsyrk)
 };
 
 constexpr int kCmsWarps = 4;
@@ -136,6 +137,13 @@ __global__ void __launch_bounds__(32 * kCmsWarps, MT >= 3 ? 3 : (MT == 2 ? 5 : 9
         cv[J][I][0] = cv[J][I][1] = 0.0;
         if (!use_c || j >= n || i >= m) continue;
         const double* cp = c + i + (long long)j * P.ldc;
+        const bool in0 = P.uplo == 0 || (P.uplo == 1 ? i >= j : i <= j);
+        const bool in1 = P.uplo == 0 || (P.uplo == 1 ? i + 1 >= j : i + 1 <= j);
+        if (!(in0 && in1)) {  // the pair straddles the diagonal (or lies outside): element-wise
+          if (in0) cv[J][I][0] = cp[0];
+          if (in1 && i + 1 < m) cv[J][I][1] = cp[1];
+          continue;
+        }
         if (P.vec && i + 1 < m) {
           const double2 v = *reinterpret_cast<const double2*>(cp);
           cv[J][I][0] = v.x;
@@ -155,6 +163,13 @@ __global__ void __launch_bounds__(32 * kCmsWarps, MT >= 3 ? 3 : (MT == 2 ? 5 : 9
         const bool two = i + 1 < m;
         const double r0 = use_c ? fma(P.alpha, acc[J][I][0], P.beta * cv[J][I][0]) : acc[J][I][0] * P.alpha;
         const double r1 = use_c ? fma(P.alpha, acc[J][I][1], P.beta * cv[J][I][1]) : acc[J][I][1] * P.alpha;
+        const bool in0 = P.uplo == 0 || (P.uplo == 1 ? i >= j : i <= j);
+        const bool in1 = P.uplo == 0 || (P.uplo == 1 ? i + 1 >= j : i + 1 <= j);
+        if (!(in0 && in1)) {
+          if (in0) cp[0] = r0;
+          if (in1 && two) cp[1] = r1;
+          continue;
+        }
         if (P.vec && two) {
           *reinterpret_cast<double2*>(cp) = make_double2(r0, r1);
         } else {
@@ -201,9 +216,9 @@ bool gemm_cmsmall_ok(int m, int n) {
 
 cudaError_t gemm_cmsmall_launch(int ta, int tb, int m, int n, int k, double alpha, const double* a, int lda,
                                 long long sa, const double* b, int ldb, long long sb, double beta, double* c,
-                                int ldc, long long sc, long long batch, cudaStream_t s) {
+                                int ldc, long long sc, int uplo, long long batch, cudaStream_t s) {
   if (batch <= 0) return cudaSuccess;
-  CmSmallArgs P{a, b, c, sa, sb, sc, lda, ldb, ldc, m, n, k, ta, tb, alpha, beta, batch, 0};
+  CmSmallArgs P{a, b, c, sa, sb, sc, lda, ldb, ldc, m, n, k, ta, tb, alpha, beta, batch, 0, uplo};
   P.vec = (reinterpret_cast<uintptr_t>(c) & 15) == 0 && ldc % 2 == 0 && sc % 2 == 0;
   const int mx = m > n ? m : n;
   if (mx <= 8) return cmsmall_t<1>(P, s);

@@ -69,9 +69,10 @@ cudaError_t gemm_cm_launch(int s, double alpha, const double* a, const double* b
 // column-major small problems, m, n <= 32, any k / trans / leading dimensions: warp per problem
 // (gemm_cmsmall.cu) — the small-n branch of the size switch (variant D, gemm.hpp:190-204)
 bool gemm_cmsmall_ok(int m, int n);
+// uplo: 0 full, 1 lower, 2 upper — the opposite triangle is neither read nor written (dsyrk)
 cudaError_t gemm_cmsmall_launch(int ta, int tb, int m, int n, int k, double alpha, const double* a, int lda,
                                 long long sa, const double* b, int ldb, long long sb, double beta, double* c,
-                                int ldc, long long sc, long long batch, cudaStream_t s);
+                                int ldc, long long sc, int uplo, long long batch, cudaStream_t s);
 
 }  // namespace pbg
 

@@ -378,7 +378,7 @@ static int dgemm_impl(const char* routine, bool batched, char transa, char trans
                          // small-n branch (variant D's role): a warp per problem, no 64x64 tile padding
                          if (gemm_cmsmall_ok(m, n))
                            return gemm_cmsmall_launch(ta != 0, tb != 0, m, n, k, alpha, (const double*)p[0], lda, sa,
-                                                      (const double*)p[1], ldb, sb, beta, o.d, ldc, sc, nb, s);
+                                                      (const double*)p[1], ldb, sb, beta, o.d, ldc, sc, 0, nb, s);
                          GemmLaunch g;
                          // M side: op(A)(i, l); N side: op(B)(l, j) as (x = j, l).
                          g.lay_a = ta == 0 ? L_MNC : L_KC;
@@ -446,6 +446,10 @@ static int dsyrk_impl(bool batched, char uplo, char trans, int n, int k, double 
                          o.vec = aligned16(p[1]) && sc % 2 == 0 && ldc % 2 == 0;
                          int up = lo ? 1 : 2;
                          if (scale_only) return scale_launch(0, o, n, n, beta, up, nb, s);
+                         // small-n branch: C = alpha op(A) op(A)^T + beta C on a warp per problem
+                         if (gemm_cmsmall_ok(n, n))
+                           return gemm_cmsmall_launch(tr != 0, tr == 0, n, n, k, alpha, (const double*)p[0], lda, sa,
+                                                      (const double*)p[0], lda, sa, beta, o.d, ldc, sc, up, nb, s);
                          GemmLaunch g;
                          g.lay_a = g.lay_b = tr == 0 ? L_MNC : L_KC;
                          g.a = g.b = cm_side(p[0], sa, lda, tr == 0, n, k);

@@ -250,6 +250,41 @@ def test_dsyrk(pb, orc, uplo, trans):
         assert same_bits(got[tri], c[tri])  # opposite triangle untouched
 
 
+@pytest.mark.parametrize("uplo", ["l", "u"])
+@pytest.mark.parametrize("trans", ["n", "t"])
+@pytest.mark.parametrize("nk", [(4, 4), (8, 3), (16, 40), (23, 17), (32, 32)])
+def test_dsyrk_small_batched(pb, orc, cuda, uplo, trans, nk):
+    """dsyrk at n <= 32 (the warp-per-problem small-n branch): both triangles and trans, padded
+    leading dimensions, beta = 0 with NaN in the stored triangle; the opposite triangle untouched."""
+    import torch
+    n, k = nk
+    rng = np.random.default_rng(n * 100 + k)
+    batch = 19
+    ar, ac = (n, k) if trans == "n" else (k, n)
+    tri = np.tril(np.ones((n, n), bool)) if uplo == "l" else np.triu(np.ones((n, n), bool))
+    for (pa, pc, alpha, beta) in [(0, 0, 1.0, 1.0), (3, 1, -0.5, 0.0), (2, 2, 1.25, -2.0)]:
+        lda, ldc = ar + pa, n + pc
+        A = rng.uniform(-1, 1, (batch, ac, lda))
+        C = rng.uniform(-1, 1, (batch, n, ldc))
+        if beta == 0.0:  # NaN in the triangle dsyrk overwrites (never read)
+            Cv = C[:, :, :n]              # [p, j, i]
+            Cv[:, tri.T] = np.nan
+        dA, dC = torch.from_numpy(A.copy()).to(cuda), torch.from_numpy(C.copy()).to(cuda)
+        r = pb.dsyrk_batched(uplo, trans, n, k, alpha, dA, lda, lda * ac, beta, dC, ldc, ldc * n, batch)
+        assert r.info == 0
+        got = dC.cpu().numpy()
+        for p in range(batch):
+            a = F(A[p].T)
+            c0 = F(C[p].T)
+            want = c0.copy(order="F")
+            orc.dsyrk(ch(uplo), ch(trans), n, k, alpha, ptr(a), lda, beta, ptr(want), ldc)
+            g, w = got[p].T[:n], want[:n]
+            assert not np.isnan(g[tri]).any()
+            assert np.linalg.norm(g[tri] - w[tri]) <= tol(k) * max(np.linalg.norm(w[tri]), 1e-300)
+            assert same_bits(g[~tri], c0[:n][~tri])        # opposite triangle untouched
+            assert same_bits(got[p].T[n:], c0[n:])          # pad rows untouched
+
+
 def test_syrk_nd(pb, orc):
     rng = np.random.default_rng(41)
     for (n, k) in [(13, 7), (64, 64), (96, 20)]:
