@@ -103,15 +103,14 @@ struct KParams {
   long long items;
   int nstages;
   const int* skip;
+  int stagger;  // cycles the second consumer warp of every scheduler partition starts late (see the consumers)
 };
 
-__device__ __forceinline__ void decode_item(const KParams& P, long long item, int& p, int& tm,
-                                            int& tn) {
-  p = (int)(item / P.tiles_per_problem);
-  int r = (int)(item - (long long)p * P.tiles_per_problem);
+// tile r of a problem -> (tm, tn)
+__device__ __forceinline__ void tile_of(const KParams& P, int r, int& tm, int& tn) {
   if (P.uplo == 0) {
-    tm = r % P.tiles_m;
-    tn = r / P.tiles_m;
+    tn = (unsigned)r / (unsigned)P.tiles_m;
+    tm = r - tn * P.tiles_m;
   } else {
     // triangular tile enumeration: r -> (hi, lo) with hi >= lo
     int hi = (int)((sqrtf(8.0f * r + 1.0f) - 1.0f) * 0.5f);
@@ -121,6 +120,27 @@ __device__ __forceinline__ void decode_item(const KParams& P, long long item, in
     if (P.uplo == 1) { tm = hi; tn = lo; } else { tm = lo; tn = hi; }
   }
 }
+
+// A CTA's walk over its items (item = blockIdx.x + i * gridDim.x) as (problem,
+// tile-in-problem), advanced without the 64-bit division per item.
+struct ItemCursor {
+  long long item;
+  int p, r, dq, dr, tpp;
+  __device__ __forceinline__ void init(const KParams& P) {
+    tpp = P.tiles_per_problem;
+    dq = (int)(gridDim.x / (unsigned)tpp);
+    dr = (int)(gridDim.x - (unsigned)dq * (unsigned)tpp);
+    item = blockIdx.x;
+    p = (int)(blockIdx.x / (unsigned)tpp);
+    r = (int)(blockIdx.x - (unsigned)p * (unsigned)tpp);
+  }
+  __device__ __forceinline__ void next() {
+    item += gridDim.x;
+    p += dq;
+    r += dr;
+    if (r >= tpp) { r -= tpp; ++p; }
+  }
+};
 
 __device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
                                          int c3, int rank, uint64_t* bar) {
@@ -240,9 +260,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
     constexpr uint32_t BYTES_A = TA::SIZE * 8, BYTES_B = TB::SIZE * 8;
     int stage = 0;
     uint32_t phase = 0;
-    for (long long item = blockIdx.x; item < P.items; item += gridDim.x) {
-      int p, tm, tn;
-      decode_item(P, item, p, tm, tn);
+    ItemCursor cur;
+    for (cur.init(P); cur.item < P.items; cur.next()) {
+      const int p = cur.p;
+      int tm, tn;
+      tile_of(P, cur.r, tm, tn);
       if (P.skip && P.skip[p]) continue;
       const int i0 = tm * TM, j0 = tn * TN;
       const int mvalid = min(TM, P.m - i0), nvalid = min(TN, P.n - j0);
@@ -281,15 +303,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
   const int g = lane >> 2, t = lane & 3;
   const int jb = (warp / NWR) * 8 * WF, ib = (warp % NWR) * 8 * WH;
   const bool use_c = P.beta != 0.0;
+  // fragment (f, h) of an interior tile sits at a fixed element offset from the
+  // lane's first pair: f * sf + h * sh (no per-element bounds or index math)
+  const long long sfc = OUT_PM ? 32 : 8LL * P.o.ldc, shc = OUT_PM ? 8LL * P.o.ldc : 8;
+  const long long sfd = OUT_PM ? 32 : 8LL * P.o.ldd, shd = OUT_PM ? 8LL * P.o.ldd : 8;
+  // a tile whose 64 x 64 elements are all written with 16-byte pairs
+  auto interior = [&](int tm, int tn) {
+    return P.o.vec && (tm + 1) * TM <= P.m && (tn + 1) * TN <= P.n &&
+           (P.uplo == 0 || (P.uplo == 1 ? tm > tn : tm < tn));
+  };
   // beta*C operands for this lane's 4x2 fragments, prefetched one item ahead
   // so their DRAM latency hides behind a whole item of tensor-core work.
   double cv[WF][WH][2], cn[WF][WH][2];
-  auto load_c = [&](long long it, double (&dst)[WF][WH][2]) {
-    int p, tm, tn;
-    decode_item(P, it, p, tm, tn);
+  auto load_c = [&](int p, int tm, int tn, double (&dst)[WF][WH][2]) {
     const double* cbase =
         P.o.c + (P.o.offs_c ? P.o.offs_c[p] : P.o.offs ? P.o.offs[p] : (long long)p * P.o.sc);
     const bool live = !(P.skip && P.skip[p]);
+    if (live && interior(tm, tn)) {
+      const double* cp0 = cbase + out_off<OUT_PM>(P.o.ldc, tm * TM + ib + 2 * t, tn * TN + jb + g);
+#pragma unroll
+      for (int f = 0; f < WF; ++f)
+#pragma unroll
+        for (int h = 0; h < WH; ++h) {
+          const double2 v = *reinterpret_cast<const double2*>(cp0 + f * sfc + h * shc);
+          dst[f][h][0] = v.x;
+          dst[f][h][1] = v.y;
+        }
+      return;
+    }
 #pragma unroll
     for (int f = 0; f < WF; ++f)
 #pragma unroll
@@ -309,18 +350,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
         }
       }
   };
-  if (use_c && blockIdx.x < P.items) load_c(blockIdx.x, cn);
+  // The two consumer warps of a scheduler partition (warp w and w + 4) would
+  // otherwise walk the stages in lockstep and reach their epilogues together,
+  // leaving the partition's FP64 tensor pipe idle for the whole epilogue.  The
+  // second warp starts late once; the offset then persists (while one warp is
+  // in its epilogue the other has the pipe alone), so one warp's epilogue runs
+  // under the other's DMMAs.
+  if (P.stagger && warp >= NCW / 2) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < P.stagger) {}
+  }
+  ItemCursor cur;
+  cur.init(P);
+  int tm = 0, tn = 0, tmn = 0, tnn = 0;
+  if (cur.item < P.items) {
+    tile_of(P, cur.r, tmn, tnn);
+    if (use_c) load_c(cur.p, tmn, tnn, cn);
+  }
   int stage = 0;
   uint32_t phase = 0;
-  for (long long item = blockIdx.x; item < P.items; item += gridDim.x) {
-    int p, tm, tn;
-    decode_item(P, item, p, tm, tn);
+  while (cur.item < P.items) {
+    const int p = cur.p;
+    tm = tmn;
+    tn = tnn;
+    cur.next();
+    const bool more = cur.item < P.items;
+    if (more) tile_of(P, cur.r, tmn, tnn);
     if (use_c) {
 #pragma unroll
       for (int f = 0; f < WF; ++f)
 #pragma unroll
         for (int h = 0; h < WH; ++h) { cv[f][h][0] = cn[f][h][0]; cv[f][h][1] = cn[f][h][1]; }
-      if (item + gridDim.x < P.items) load_c(item + gridDim.x, cn);
+      if (more) load_c(cur.p, tmn, tnn, cn);
     }
     if (P.skip && P.skip[p]) continue;
     const int i0 = tm * TM, j0 = tn * TN;
@@ -375,6 +436,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
     }
 
     // Epilogue: d = alpha*acc + beta*c, masked to the problem and the uplo triangle.
+    if (interior(tm, tn)) {
+      double* dp0 = dbase + out_off<OUT_PM>(P.o.ldd, i0 + ib + 2 * t, j0 + jb + g);
+#pragma unroll
+      for (int f = 0; f < WF; ++f)
+#pragma unroll
+        for (int h = 0; h < WH; ++h) {
+          const double r0 = use_c ? fma(P.alpha, acc[f][h][0], P.beta * cv[f][h][0]) : acc[f][h][0] * P.alpha;
+          const double r1 = use_c ? fma(P.alpha, acc[f][h][1], P.beta * cv[f][h][1]) : acc[f][h][1] * P.alpha;
+          *reinterpret_cast<double2*>(dp0 + f * sfd + h * shd) = make_double2(r0, r1);
+        }
+      continue;
+    }
 #pragma unroll
     for (int f = 0; f < WF; ++f)
 #pragma unroll
@@ -515,6 +588,14 @@ cudaError_t gemm_launch(const GemmLaunch& g, cudaStream_t s) {
   P.beta = g.beta;
   P.uplo = g.uplo;
   P.skip = g.skip;
+  {
+    // PBGPU_ENGINE_STAGGER=<cycles> (tuning; 0 = lockstep consumers)
+    static const int stagger = [] {
+      const char* e = getenv("PBGPU_ENGINE_STAGGER");
+      return e ? atoi(e) : 0;
+    }();
+    P.stagger = stagger;
+  }
   P.tiles_m = (g.m + TM - 1) / TM;
   P.tiles_n = (g.n + TN - 1) / TN;
   if (g.uplo) {
