@@ -39,13 +39,10 @@
 namespace pbg {
 
 constexpr int TM = 64, TN = 64, BK = 32;
-#ifndef PB_ENGINE_WH
-#define PB_ENGINE_WH 2
-#endif
 // warp tile: WH row tiles x WF column tiles of 8x8 (of D' = C^T); measured: WH = 4
 // (four 32x32-tile warps, half the fragment loads per DMMA) is 25 % slower than
 // eight 32x16-tile warps (WH = 2) at every compute-bound size
-constexpr int WH = PB_ENGINE_WH, WF = 4;
+constexpr int WH = 2, WF = 4;
 constexpr int NWR = TM / (8 * WH);                 // warps along the tile's rows
 constexpr int NCW = NWR * (TN / (8 * WF));         // consumer warps
 constexpr int NTHREADS = (NCW + 1) * 32;
@@ -232,7 +229,63 @@ __device__ __forceinline__ long long out_off(int ld, int i, int j) {
   return (long long)i + (long long)j * ld;
 }
 
-template <int LA, int LB, int OUT_PM>
+// One item's k loop for a warp whose tile has FA x HA live 8x8 fragments (the
+// others lie wholly outside m x n or the uplo triangle and stay zero): only
+// the live fragments are loaded and multiplied.  Every warp, live or not,
+// waits for each stage and releases it, so the ring's phases stay in step.
+template <int FA, int HA, class TA, class TB>
+__device__ __forceinline__ void engine_k_loop(const KParams& P, const double* smem, uint64_t* full, uint64_t* empty,
+                                              int stage_doubles, int& stage, uint32_t& phase, int ib, int jb, int g,
+                                              int t, int lane, double (&acc)[WF][WH][2]) {
+  for (int kc = 0; kc < P.nk; ++kc) {
+    const int kvalid = min(BK, P.k - kc * BK);
+    mbar_wait(&full[stage], phase);
+    const double* sA = smem + (size_t)stage * stage_doubles;
+    const double* sB = sA + TA::SIZE;
+    if constexpr (FA > 0 && HA > 0) {
+      if (kvalid == BK) {
+#pragma unroll
+        for (int ks = 0; ks < BK / 4; ++ks) {
+          const int l = ks * 4 + t;
+          double av[FA], bv[HA];
+#pragma unroll
+          for (int f = 0; f < FA; ++f) av[f] = sB[TB::at(jb + f * 8 + g, l)];
+#pragma unroll
+          for (int h = 0; h < HA; ++h) bv[h] = sA[TA::at(ib + h * 8 + g, l)];
+#pragma unroll
+          for (int f = 0; f < FA; ++f)
+#pragma unroll
+            for (int h = 0; h < HA; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
+        }
+      } else {
+        // Tail chunk: lanes past k contribute exact zeros whatever the stage
+        // holds (pad lanes of panel-major operands are unspecified data).
+        const int ksteps = (kvalid + 3) >> 2;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const int l = ks * 4 + t;
+          const bool in = l < kvalid;
+          double av[FA], bv[HA];
+#pragma unroll
+          for (int f = 0; f < FA; ++f) av[f] = in ? sB[TB::at(jb + f * 8 + g, l)] : 0.0;
+#pragma unroll
+          for (int h = 0; h < HA; ++h) bv[h] = in ? sA[TA::at(ib + h * 8 + g, l)] : 0.0;
+#pragma unroll
+          for (int f = 0; f < FA; ++f)
+#pragma unroll
+            for (int h = 0; h < HA; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == P.nstages) { stage = 0; phase ^= 1; }
+  }
+}
+
+// EDGE = 1: launches with ragged tiles (m or n not a multiple of 64) or an uplo
+// mask pick each warp's live fragments per item; EDGE = 0 (every tile full)
+// keeps the plain loop — the per-item dispatch measured 4 % slower at k = 128.
+template <int LA, int LB, int OUT_PM, int EDGE>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_constant__ KParams P) {
   using TA = LayT<LA>;
   using TB = LayT<LB>;
@@ -301,7 +354,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
 
   // -------------------------------------------------------------- consumers
   const int g = lane >> 2, t = lane & 3;
-  const int jb = (warp / NWR) * 8 * WF, ib = (warp % NWR) * 8 * WH;
+  // warps w and w + 4 share a scheduler partition: with ragged tiles the second
+  // half takes its row blocks rotated by two, so the live warps of an edge tile
+  // (few valid rows) fall on different partitions, and the warps a diagonal
+  // syrk tile skips (0, 1 lower / 4, 5 upper) sit on the producer warp's
+  const int jb = (EDGE ? 1 - warp / NWR : warp / NWR) * 8 * WF;
+  const int ib = ((warp + (EDGE ? 2 : 0) * (warp / NWR)) % NWR) * 8 * WH;
   const bool use_c = P.beta != 0.0;
   // fragment (f, h) of an interior tile sits at a fixed element offset from the
   // lane's first pair: f * sf + h * sh (no per-element bounds or index math)
@@ -393,47 +451,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
 #pragma unroll
       for (int h = 0; h < WH; ++h) acc[f][h][0] = acc[f][h][1] = 0.0;
 
-    for (int kc = 0; kc < P.nk; ++kc) {
-      const int kvalid = min(BK, P.k - kc * BK);
-      mbar_wait(&full[stage], phase);
-      const double* sA = smem + (size_t)stage * STAGE;
-      const double* sB = sA + TA::SIZE;
-      if (kvalid == BK) {
-#pragma unroll
-        for (int ks = 0; ks < BK / 4; ++ks) {
-          const int l = ks * 4 + t;
-          double av[WF], bv[WH];
-#pragma unroll
-          for (int f = 0; f < WF; ++f) av[f] = sB[TB::at(jb + f * 8 + g, l)];
-#pragma unroll
-          for (int h = 0; h < WH; ++h) bv[h] = sA[TA::at(ib + h * 8 + g, l)];
-#pragma unroll
-          for (int f = 0; f < WF; ++f)
-#pragma unroll
-            for (int h = 0; h < WH; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
-        }
-      } else {
-        // Tail chunk: lanes past k contribute exact zeros whatever the stage
-        // holds (pad lanes of panel-major operands are unspecified data).
-        const int ksteps = (kvalid + 3) >> 2;
-        for (int ks = 0; ks < ksteps; ++ks) {
-          const int l = ks * 4 + t;
-          const bool in = l < kvalid;
-          double av[WF], bv[WH];
-#pragma unroll
-          for (int f = 0; f < WF; ++f) av[f] = in ? sB[TB::at(jb + f * 8 + g, l)] : 0.0;
-#pragma unroll
-          for (int h = 0; h < WH; ++h) bv[h] = in ? sA[TA::at(ib + h * 8 + g, l)] : 0.0;
-#pragma unroll
-          for (int f = 0; f < WF; ++f)
-#pragma unroll
-            for (int h = 0; h < WH; ++h) dmma(acc[f][h][0], acc[f][h][1], av[f], bv[h]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == P.nstages) { stage = 0; phase ^= 1; }
+#define PB_KL(F, H) \
+  engine_k_loop<F, H, TA, TB>(P, smem, full, empty, STAGE, stage, phase, ib, jb, g, t, lane, acc)
+    if constexpr (!EDGE) {
+      PB_KL(WF, WH);
+    } else {
+      // live fragments of this warp's tile: those with an element inside m x n;
+      // on a diagonal syrk tile a warp wholly in the opposite triangle has none
+      static_assert(WH == 2 && WF == 4, "the live-fragment dispatch is written for 4 x 2 fragments");
+      int ha = min(WH, max(0, (P.m - i0 - ib + 7) >> 3)), fa = min(WF, max(0, (P.n - j0 - jb + 7) >> 3));
+      if (P.uplo && tm == tn && (P.uplo == 1 ? ib + 8 * WH - 1 < jb : jb + 8 * WF - 1 < ib)) fa = 0;
+      if (ha == 0) fa = 0;
+      if (fa == WF && ha == WH) PB_KL(4, 2);
+      else if (fa == 0) PB_KL(0, 0);
+      else if (ha == 2) { if (fa == 3) PB_KL(3, 2); else if (fa == 2) PB_KL(2, 2); else PB_KL(1, 2); }
+      else { if (fa == 4) PB_KL(4, 1); else if (fa == 3) PB_KL(3, 1); else if (fa == 2) PB_KL(2, 1); else PB_KL(1, 1); }
     }
+#undef PB_KL
 
     // Epilogue: d = alpha*acc + beta*c, masked to the problem and the uplo triangle.
     if (interior(tm, tn)) {
@@ -555,8 +589,8 @@ static bool make_map(CUtensorMap* tm, int lay, const OpDesc& d, int xdim, int k,
   return r == CUDA_SUCCESS;
 }
 
-template <int LA, int LB, int OUT_PM>
-static cudaError_t launch_t(KParams& P, cudaStream_t s) {
+template <int LA, int LB, int OUT_PM, int EDGE>
+static cudaError_t launch_e(KParams& P, cudaStream_t s) {
   constexpr int STAGE = LayT<LA>::SIZE + LayT<LB>::SIZE;
   const size_t stage_bytes = (size_t)STAGE * 8;
   const size_t budget = 227 * 1024 - 256;
@@ -564,14 +598,21 @@ static cudaError_t launch_t(KParams& P, cudaStream_t s) {
   nst = std::min(nst, 8);
   P.nstages = nst;
   size_t smem = (size_t)nst * stage_bytes + (size_t)nst * 16;
-  auto kern = gemm_tiles_kernel<LA, LB, OUT_PM>;
+  auto kern = gemm_tiles_kernel<LA, LB, OUT_PM, EDGE>;
   {
     cudaError_t e = smem_attr((const void*)kern, (int)smem);
     if (e != cudaSuccess) return e;
   }
   long long grid = std::min<long long>(P.items, (long long)num_sms());
+  if (P.items < 8 * grid) P.stagger = 0;
   kern<<<(int)grid, NTHREADS, smem, s>>>(P);
   return cudaGetLastError();
+}
+
+template <int LA, int LB, int OUT_PM>
+static cudaError_t launch_t(KParams& P, cudaStream_t s) {
+  const bool ragged = (P.m % TM) != 0 || (P.n % TN) != 0 || P.uplo != 0;
+  return ragged ? launch_e<LA, LB, OUT_PM, 1>(P, s) : launch_e<LA, LB, OUT_PM, 0>(P, s);
 }
 
 cudaError_t gemm_launch(const GemmLaunch& g, cudaStream_t s) {
@@ -589,10 +630,11 @@ cudaError_t gemm_launch(const GemmLaunch& g, cudaStream_t s) {
   P.uplo = g.uplo;
   P.skip = g.skip;
   {
-    // PBGPU_ENGINE_STAGGER=<cycles> (tuning; 0 = lockstep consumers)
+    // consumer offset in cycles (PBGPU_ENGINE_STAGGER overrides; 0 = lockstep);
+    // measured +1 % at s >= 128, only worth its start-up delay on long item lists
     static const int stagger = [] {
       const char* e = getenv("PBGPU_ENGINE_STAGGER");
-      return e ? atoi(e) : 0;
+      return e ? atoi(e) : 6000;
     }();
     P.stagger = stagger;
   }

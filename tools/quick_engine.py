@@ -46,7 +46,7 @@ for n in (128, 256):
     out.append(f"cm{n} {ms:.4f}ms {fl / ms / 1e9 / (PEAK / 1e12):.3f}")
     del A, B, C
 R = pb.PanelRef
-for s in (112, 128, 132, 192, 256, 320):
+for s in (100, 104, 108, 112, 116, 124, 128, 132, 160, 192, 196, 256, 260, 320):
     batch = (2 ** 31) // (32 * s * s)
     L = s * s
     A = torch.rand((batch, L), device=dev, dtype=torch.float64)
