@@ -81,7 +81,8 @@ cudaError_t syrk_potrf_launch(const SyrkPotrfLaunch& L, cudaStream_t s) {
   g.b.base = L.b; g.b.stride = L.sb; g.b.ld = L.cnb;
   g.b.bulk = ((reinterpret_cast<uintptr_t>(L.b) & 15) == 0) && (L.offs ? L.offs_even != 0 : L.sb % 2 == 0);
   g.o.c = L.c; g.o.d = L.d; g.o.sc = L.sc; g.o.sd = L.sd; g.o.ldc = L.cnc; g.o.ldd = L.cnd;
-  g.o.vec = 0;
+  g.o.vec = ((reinterpret_cast<uintptr_t>(L.c) & 15) == 0) && ((reinterpret_cast<uintptr_t>(L.d) & 15) == 0) &&
+            (L.offs ? L.offs_even != 0 : (L.sc % 2 == 0 && L.sd % 2 == 0));  // pm pairs (i, i + 1), i even
   g.a.offs = g.b.offs = g.o.offs = L.offs;
   g.m = g.n = L.n;
   g.k = L.k;
@@ -106,6 +107,15 @@ static bool chain_unfused() {
   static const bool v = [] {
     const char* e = getenv("PBGPU_CHAIN_UNFUSED");
     return e && e[0] == '1';
+  }();
+  return v;
+}
+
+// PBGPU_CHAIN_CM_INPLACE=0: column-major large orders through the strided workspace (A/B only)
+static bool cm_inplace_on() {
+  static const bool v = [] {
+    const char* e = getenv("PBGPU_CHAIN_CM_INPLACE");
+    return !(e && e[0] == '0');
   }();
   return v;
 }
@@ -248,7 +258,17 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
   // allocated here on the caller's stream — large stream-ordered allocations issued
   // concurrently from several streams made the pool serialise or grow (cm 32 -> 49 ms)
   double* ws_stream[kChainStreams] = {};
-  if (!L.pm && !big.empty()) {
+  // 16-byte aligned column-major problems take the panel-major route below: in
+  // place on the caller's buffers through the offsets (tensor maps with offset
+  // dimensions in the engine), no workspace, gather or scatter
+  bool cm_inplace = !L.pm && cm_inplace_on() && (reinterpret_cast<uintptr_t>(L.A) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
+  for (auto& kv : big) {
+    if (!cm_inplace) break;
+    cm_inplace = kv.first % 2 == 0;
+    for (int q : kv.second) cm_inplace = cm_inplace && ov[q] % 2 == 0;
+  }
+  if (!L.pm && !cm_inplace && !big.empty()) {
     size_t need[kChainStreams] = {};
     int k = 0;
     for (auto it = big.rbegin(); it != big.rend(); ++it, k = (k + 1) % nstreams)
@@ -281,18 +301,36 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
     cudaMemcpyAsync(d_o, ob.data(), sizeof(long long) * cnt, cudaMemcpyHostToDevice, s);
     double* wc = nullptr;  // column-major: the factor's workspace (S = C + A A^T, then L)
     double* wa = nullptr;
-    if (!L.pm) {
-      // column-major: the engine's tensor-map path needs strided operands (its
-      // per-column bulk copies measured 1.7x slower here), so A is gathered once,
-      // S = C + A A^T lands in a strided workspace (C read through the offsets),
-      // is factored there, and only L's lower triangle goes back to C
+    if (cm_inplace) {
+      GemmLaunch g;  // dsyrk('l','n') in place: C += A A^T (lower)
+      g.lay_a = g.lay_b = L_MNC;
+      g.a.base = g.b.base = L.A; g.a.offs = g.b.offs = d_o; g.a.ld = g.b.ld = n; g.a.bulk = g.b.bulk = 1;
+      g.o.c = L.C; g.o.d = L.C; g.o.offs = d_o; g.o.ldc = g.o.ldd = n; g.o.vec = 1;
+      g.m = g.n = g.k = n;
+      g.alpha = 1.0; g.beta = 1.0; g.uplo = 1; g.batch = cnt;
+      e = gemm_launch(g, s);
+      if (e == cudaSuccess) {
+        PotrfLaunch P;
+        P.a = L.C; P.offs = d_o; P.offs_even = 1; P.lda = n; P.n = n; P.info = w_info; P.batch = cnt;
+        e = potrf_launch(P, s);
+      }
+    } else if (!L.pm) {
+      // column-major: A streams straight from the caller's buffer through the
+      // engine's offset tensor maps (16-byte aligned problems; otherwise it is
+      // gathered into the strided workspace first), S = C + A A^T lands in a
+      // strided workspace (C read through the offsets), is factored there, and
+      // only L's lower triangle goes back to C
       const long long nn = (long long)n * n;
       wa = ws_stream[pool ? stream_slot : 0];
       wc = wa + nn * cnt;
-      gather_kernel<<<grid2(nn, cnt), 256, 0, s>>>(L.A, d_o, wa, n);
       GemmLaunch g;  // dsyrk('l','n'): S = C + A A^T
       g.lay_a = g.lay_b = L_MNC;
-      g.a.base = g.b.base = wa; g.a.stride = g.b.stride = nn; g.a.ld = g.b.ld = n; g.a.bulk = g.b.bulk = 1;
+      if (even && n % 2 == 0 && (reinterpret_cast<uintptr_t>(L.A) & 15) == 0) {
+        g.a.base = g.b.base = L.A; g.a.offs = g.b.offs = d_o; g.a.ld = g.b.ld = n; g.a.bulk = g.b.bulk = 1;
+      } else {
+        gather_kernel<<<grid2(nn, cnt), 256, 0, s>>>(L.A, d_o, wa, n);
+        g.a.base = g.b.base = wa; g.a.stride = g.b.stride = nn; g.a.ld = g.b.ld = n; g.a.bulk = g.b.bulk = 1;
+      }
       g.o.c = L.C; g.o.offs_c = d_o; g.o.d = wc; g.o.sd = nn; g.o.ldc = g.o.ldd = n;
       g.o.vec = even && n % 2 == 0 && (reinterpret_cast<uintptr_t>(L.C) & 15) == 0;
       g.m = g.n = g.k = n;
@@ -321,7 +359,8 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
       T.lower = 1; T.trans = 1; T.unit = 0;
       T.mm = T.nn = n;
       T.alpha = 1.0;
-      T.a = L.pm ? L.C : wc; T.offs_a = L.pm ? d_o : nullptr; T.sa = (long long)n * n; T.lda = n;
+      const bool in_c = L.pm || cm_inplace;
+      T.a = in_c ? L.C : wc; T.offs_a = in_c ? d_o : nullptr; T.sa = (long long)n * n; T.lda = n;
       T.b = L.B; T.ldb = n;
       T.d = L.B; T.ldd = n;
       T.offs_b = d_o;
@@ -330,7 +369,7 @@ cudaError_t chain_launch(const ChainLaunch& L, cudaStream_t s0) {
       T.batch = cnt;
       e = trsm_launch(T, s);
     }
-    if (e == cudaSuccess && !L.pm) {
+    if (e == cudaSuccess && !L.pm && !cm_inplace) {
       scatter_lower_kernel<<<grid2((long long)n * n, cnt), 256, 0, s>>>(wc, L.C, d_o, n);
       e = cudaGetLastError();
     }

@@ -92,7 +92,7 @@ struct KParams {
   OutDesc o;
   int tmaA, tmaB;
   int bulkA, bulkB;                // per-problem offsets: column / panel bulk copies instead of a tensor map
-  int batched_mapA, batched_mapB;  // tensor map has a problem dimension
+  int batched_mapA, batched_mapB;  // 1: the tensor map has a problem dimension, 2: per-problem offset dimensions
   int m, n, k;
   double alpha, beta;
   int uplo;
@@ -139,38 +139,56 @@ struct ItemCursor {
   }
 };
 
-__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
-                                         int c3, int rank, uint64_t* bar) {
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* tm, const int (&c)[5], int rank,
+                                         uint64_t* bar) {
   const uint64_t desc = reinterpret_cast<uint64_t>(tm);
+  const uint32_t d = smem_u32(dst), b = smem_u32(bar);
   if (rank == 3)
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
-        "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(d), "l"(desc), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(b)
         : "memory");
   else if (rank == 4)
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
-        "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(d), "l"(desc), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]),
+        "r"(b)
+        : "memory");
+  else if (rank == 5)
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(d), "l"(desc), "r"(c[0]), "r"(c[1]), "r"(c[2]),
+        "r"(c[3]), "r"(c[4]), "r"(b)
         : "memory");
   else
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
-        "l"(desc), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(d), "l"(desc), "r"(c[0]), "r"(c[1]), "r"(b)
         : "memory");
 }
 
 // Producer, TMA path: one tensor copy for this side's chunk (lane 0).
+// Coordinates innermost first.  mode 1: the map has a problem dimension
+// (uniform stride); mode 2: per-problem element offsets — the map carries two
+// extra dimensions of 16-byte and 16-MiB stride whose coordinates spell the
+// (even) offset, so offset batches stream through the same tensor copies.
 template <int L>
-__device__ __forceinline__ void tma_side(const CUtensorMap* tm, int batched, int p, int x0, int l0,
+__device__ __forceinline__ void tma_side(const CUtensorMap* tm, int mode, int p, long long off, int x0, int l0,
                                          double* s, uint64_t* bar) {
-  // coordinates innermost first; rank includes the problem dimension when batched
-  if (L == L_MNC) tma_load(s, tm, x0, l0, batched ? p : 0, 0, batched ? 3 : 2, bar);
-  else if (L == L_KC) tma_load(s, tm, l0, x0, batched ? p : 0, 0, batched ? 3 : 2, bar);
-  else if (L == L_PMX) tma_load(s, tm, 0, l0, x0 >> 2, batched ? p : 0, batched ? 4 : 3, bar);
-  else tma_load(s, tm, 0, x0, l0 >> 2, batched ? p : 0, batched ? 4 : 3, bar);
+  int c[5] = {0, 0, 0, 0, 0};
+  int rank;
+  if (L == L_MNC) { c[0] = x0; c[1] = l0; rank = 2; }
+  else if (L == L_KC) { c[0] = l0; c[1] = x0; rank = 2; }
+  else if (L == L_PMX) { c[1] = l0; c[2] = x0 >> 2; rank = 3; }
+  else { c[1] = x0; c[2] = l0 >> 2; rank = 3; }
+  if (mode == 1) {
+    c[rank++] = p;
+  } else if (mode == 2) {
+    const long long o = off >> 1;
+    c[rank++] = (int)(o & 0xfffff);
+    c[rank++] = (int)(o >> 20);
+  }
+  tma_load(s, tm, c, rank, bar);
 }
 
 // Producer, fallback path: every (x, l) of the 64 x kvalid4 chunk through
@@ -321,6 +339,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
       if (P.skip && P.skip[p]) continue;
       const int i0 = tm * TM, j0 = tn * TN;
       const int mvalid = min(TM, P.m - i0), nvalid = min(TN, P.n - j0);
+      const long long offA = P.batched_mapA == 2 ? P.a.offs[p] : 0, offB = P.batched_mapB == 2 ? P.b.offs[p] : 0;
       for (int kc = 0; kc < P.nk; ++kc) {
         const int l0 = kc * BK, kvalid = min(BK, P.k - l0);
         mbar_wait(&empty[stage], phase ^ 1);
@@ -329,8 +348,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
         if (lane == 0) {
           const uint32_t bytes = (P.tmaA ? BYTES_A : 0) + (P.tmaB ? BYTES_B : 0);
           if (bytes) mbar_expect_tx(&full[stage], bytes);
-          if (P.tmaA) tma_side<LA>(&P.tmA, P.batched_mapA, p, i0, l0, sA, &full[stage]);
-          if (P.tmaB) tma_side<LB>(&P.tmB, P.batched_mapB, p, j0, l0, sB, &full[stage]);
+          if (P.tmaA) tma_side<LA>(&P.tmA, P.batched_mapA, p, offA, i0, l0, sA, &full[stage]);
+          if (P.tmaB) tma_side<LB>(&P.tmB, P.batched_mapB, p, offB, j0, l0, sB, &full[stage]);
         }
         if constexpr (LA == L_MNC || LA == L_PMX)
           if (P.bulkA) bulk_side<LA>(P.a, p, i0, mvalid, l0, kvalid, sA, lane, &full[stage]);
@@ -546,7 +565,7 @@ static bool make_map(CUtensorMap* tm, int lay, const OpDesc& d, int xdim, int k,
   if (!enc || !d.base) return false;
   if ((reinterpret_cast<uintptr_t>(d.base) & 15) != 0) return false;
   if (((long long)d.ld * 8) % 16 != 0) return false;
-  const bool bdim = batch > 1 && d.stride != 0;
+  const bool bdim = !d.offs && batch > 1 && d.stride != 0;
   if (bdim && (d.stride * 8) % 16 != 0) return false;
   if (xdim <= 0 || k <= 0) return false;
   cuuint64_t dims[5], strides[4];
@@ -581,11 +600,22 @@ static bool make_map(CUtensorMap* tm, int lay, const OpDesc& d, int xdim, int k,
     strides[rank - 1] = (cuuint64_t)d.stride * 8;
     box[rank] = 1;
     ++rank;
+  } else if (d.offs) {
+    // per-problem offsets (even, caller-checked through `bulk`): offset / 2 =
+    // lo + 2^20 hi as the coordinates of a 16-byte and a 16-MiB stride dimension
+    dims[rank] = 1u << 20;
+    strides[rank - 1] = 16;
+    box[rank] = 1;
+    ++rank;
+    dims[rank] = 1u << 30;
+    strides[rank - 1] = 16ull << 20;
+    box[rank] = 1;
+    ++rank;
   }
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(d.base), dims,
                    strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  *batched = bdim;
+  *batched = d.offs ? 2 : bdim ? 1 : 0;
   return r == CUDA_SUCCESS;
 }
 
@@ -653,10 +683,17 @@ cudaError_t gemm_launch(const GemmLaunch& g, cudaStream_t s) {
     const char* e = getenv("PBGPU_NO_TMA");
     return e && e[0] == '1';
   }();
-  // per-problem offsets have no tensor-map form: those sides stream by column /
-  // panel bulk copies (bulk = every problem base 16-byte aligned, caller-checked)
-  if (!no_tma && g.a.bulk && !g.a.offs) P.tmaA = make_map(&P.tmA, g.lay_a, g.a, g.m, g.k, g.batch, &P.batched_mapA);
-  if (!no_tma && g.b.bulk && !g.b.offs) P.tmaB = make_map(&P.tmB, g.lay_b, g.b, g.n, g.k, g.batch, &P.batched_mapB);
+  // per-problem offsets ride on two extra tensor-map dimensions (make_map); should the
+  // encode fail, those sides stream by column / panel bulk copies (bulk = every problem
+  // base 16-byte aligned, caller-checked).  PBGPU_OFFS_TMA=0 forces the bulk copies.
+  static const bool offs_tma = [] {
+    const char* e = getenv("PBGPU_OFFS_TMA");
+    return !(e && e[0] == '0');
+  }();
+  if (!no_tma && g.a.bulk && (!g.a.offs || offs_tma))
+    P.tmaA = make_map(&P.tmA, g.lay_a, g.a, g.m, g.k, g.batch, &P.batched_mapA);
+  if (!no_tma && g.b.bulk && (!g.b.offs || offs_tma))
+    P.tmaB = make_map(&P.tmB, g.lay_b, g.b, g.n, g.k, g.batch, &P.batched_mapB);
   auto bulk_ok = [](int lay, const OpDesc& d, int x) {
     if (!d.offs || !d.bulk) return false;
     if (lay == L_PMX) return true;

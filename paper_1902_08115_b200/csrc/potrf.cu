@@ -94,7 +94,9 @@ cudaError_t potrf_launch(const PotrfLaunch& L, cudaStream_t s) {
     g.o.d = a22;
     g.o.sc = g.o.sd = L.stride;
     g.o.ldc = g.o.ldd = L.lda;
-    g.o.vec = 0;
+    // 16-byte pairs (i, i + 1), i even: block origins are multiples of 4 rows
+    g.o.vec = ((reinterpret_cast<uintptr_t>(a22) & 15) == 0) && (L.pm || L.lda % 2 == 0) &&
+              (L.offs ? L.offs_even != 0 : L.stride % 2 == 0);
     g.m = g.n = rest;
     g.k = w;
     g.alpha = -1.0;
