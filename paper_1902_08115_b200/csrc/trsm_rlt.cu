@@ -120,7 +120,8 @@ __device__ __noinline__ void rlt_rows_exact(const TrsmLaunch& L, const double* A
 // tile loops are fully unrolled, and shared memory holds only the staged rows
 // of A, so residency is no longer bounded by 8 rows x n of X per warp.
 template <int PM, int NT>
-__global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_constant__ RltArgs R) {
+__global__ void __launch_bounds__(32 * kRltWarps, NT > 20 ? 3 : NT > 12 ? 4 : NT > 0 ? 5 : 1)
+    trsm_rlt_kernel(const __grid_constant__ RltArgs R) {  // (register caps at the residency the X tiles allow)
   extern __shared__ __align__(16) double sm_all[];
   const TrsmLaunch& L = R.L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, tid = threadIdx.x;
@@ -173,6 +174,17 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     double* ab = ab_base + (J & 1) * abs;
     const int cols = 8 * J + 8, g2 = (tid & 3) * 2, row = 8 * J + g2;
     const bool r0 = row < n, r1 = row + 1 < n;
+    if (r1 && pair_al && cols <= n) {
+      // every pair whole and aligned (all tiles but a ragged last one): one
+      // pointer pair stepped by 32 columns, no per-copy index math or checks
+      // (the generic loop below had cost half of the kernel's instructions)
+      int c = tid >> 2;
+      const double* src = A + rlt_off<PM>(lda, row, c);
+      const long long sstep = PM ? 4LL * 8 * kRltWarps : (long long)lda * 8 * kRltWarps;
+      double* dst = ab + ab_idx(c, g2);
+      for (; c < cols; c += 8 * kRltWarps, src += sstep, dst += 64 * kRltWarps) cp_async16(dst, src);
+      return;
+    }
     for (int c = tid >> 2; c < cols; c += 8 * kRltWarps) {
       double* dst = ab + ab_idx(c, g2);
       const bool v0 = r0 && c < n, v1 = r1 && c < n;
@@ -193,8 +205,11 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
   };
   bool bad = false;  // this lane saw a non-finite X
   double wn0 = R.W[p * R.ntmax * 64 + lane], wn1 = R.W[p * R.ntmax * 64 + 32 + lane];  // tile 0's inverse
-  double nb0 = (rok && 2 * t < n) ? B[xo(ldb, r, 2 * t)] : 0.0;
-  double nb1 = (rok && 2 * t + 1 < n) ? B[xo(ldb, r, 2 * t + 1)] : 0.0;
+  // this lane's right-hand sides: B(r, 8J + 2t) and its right neighbour, tile J at brow + J * bstep8
+  const double* brow = B + xo(ldb, rok ? r : 0, 2 * t);
+  const long long bstep1 = (!PM && L.twin) ? 1 : PM ? 4 : ldb, bstep8 = 8 * bstep1;
+  double nb0 = (rok && 2 * t < n) ? brow[0] : 0.0;
+  double nb1 = (rok && 2 * t + 1 < n) ? brow[bstep1] : 0.0;
 #pragma unroll
   for (int J = 0; J < (REG ? NT : 1 << 30); ++J) {
     if (J >= nt) break;
@@ -206,8 +221,8 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     const int ca = 8 * J + 2 * t, cb = ca + 1;
     double acc0 = alpha * nb0, acc1 = alpha * nb1;
     if (J + 1 < nt) {  // next tile's right-hand side, loaded under this tile's work
-      nb0 = (rok && ca + 8 < n) ? B[xo(ldb, r, ca + 8)] : 0.0;
-      nb1 = (rok && cb + 8 < n) ? B[xo(ldb, r, cb + 8)] : 0.0;
+      nb0 = (rok && ca + 8 < n) ? brow[(J + 1) * bstep8] : 0.0;
+      nb1 = (rok && cb + 8 < n) ? brow[(J + 1) * bstep8 + bstep1] : 0.0;
     }
     // ---- C -= X(:, 0:8J) A(J, 0:8J)^T ----
     double e0 = 0.0, e1 = 0.0;  // second accumulator pair: two independent DMMA chains
@@ -275,6 +290,8 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
     rlt_rows_exact<PM>(L, A, B, D, lda, ldb, ldd, n, m, rb * 8, lane);
   } else {
     // lane (g, t) holds X(r, 8J + t) and X(r, 8J + 4 + t) (A-fragment order)
+    double* drow = D + xo(ldd, rok ? r : 0, t);
+    const long long dstep1 = (!PM && L.twin) ? 1 : PM ? 4 : ldd;
 #pragma unroll
     for (int J = 0; J < (REG ? NT : 1 << 30); ++J) {
       if (J >= nt) break;
@@ -287,8 +304,8 @@ __global__ void __launch_bounds__(32 * kRltWarps) trsm_rlt_kernel(const __grid_c
         v1 = lds64(xs + 8u * ((2 * J + 1) * 32 + lane));
       }
       const int c0 = 8 * J + t, c1 = c0 + 4;
-      if (rok && c0 < n) D[xo(ldd, r, c0)] = v0;
-      if (rok && c1 < n) D[xo(ldd, r, c1)] = v1;
+      if (rok && c0 < n) drow[J * 8 * dstep1] = v0;
+      if (rok && c1 < n) drow[(J * 8 + 4) * dstep1] = v1;
     }
   }
   if (rb == 0 && lane == 0 && L.info && !L.skip_nonzero) L.info[p] = 0;
