@@ -161,6 +161,9 @@ __global__ void __launch_bounds__(32 * kRltWarps, NT > 20 ? 3 : NT > 12 ? 4 : NT
   const int r = rb * 8 + g;
   const bool rok = r < m;
   constexpr bool REG = NT > 0;
+  // right-hand sides / inverse fragments two tiles ahead: 24 more registers, which the
+  // variants sitting on their register cap (NT = 20, 32) would spill (measured slower there)
+  constexpr bool DEEP = REG && NT != 20 && NT != 32;
   const uint32_t xs = smem_u32(sm_all + (size_t)warp * R.ntmax * 64);  // [tile][kk][lane] (shared variant)
   double* ab_base = sm_all + (REG ? 0 : (size_t)kRltWarps * R.ntmax * 64);  // 2 x [8 * ntmax * 8]
   double xr[NT > 0 ? NT : 1][2];                                          // (register variant)
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(32 * kRltWarps, NT > 20 ? 3 : NT > 12 ? 4 : NT
   // thread tid always copies the pair (8J + 2(tid & 3), +1) of columns tid/4, tid/4 + 32, ...
   const bool pair_al = (reinterpret_cast<uintptr_t>(A) & 15) == 0 && (PM || lda % 2 == 0);
   auto stage = [&](int J) {
-    double* ab = ab_base + (J & 1) * abs;
+    double* ab = ab_base + (REG ? J % 3 : J & 1) * abs;
     const int cols = 8 * J + 8, g2 = (tid & 3) * 2, row = 8 * J + g2;
     const bool r0 = row < n, r1 = row + 1 < n;
     if (r1 && pair_al && cols <= n) {
@@ -197,7 +200,14 @@ __global__ void __launch_bounds__(32 * kRltWarps, NT > 20 ? 3 : NT > 12 ? 4 : NT
       }
     }
   };
+  // register variant: three row buffers, staged two tiles ahead in cp.async
+  // groups (the wait at a tile's top is for a copy issued two tiles earlier)
   stage(0);
+  if constexpr (REG) {
+    cp_async_commit();
+    if (nt > 1) stage(1);
+    cp_async_commit();
+  }
   // X(r, c) of the effective problem: B / D element (r, c), or (c, r) for a Left
   // solve run as its transposed twin (level3.hpp:300-303; column-major only)
   auto xo = [&](long long ld, int rr, int cc) -> long long {
@@ -208,21 +218,53 @@ __global__ void __launch_bounds__(32 * kRltWarps, NT > 20 ? 3 : NT > 12 ? 4 : NT
   // this lane's right-hand sides: B(r, 8J + 2t) and its right neighbour, tile J at brow + J * bstep8
   const double* brow = B + xo(ldb, rok ? r : 0, 2 * t);
   const long long bstep1 = (!PM && L.twin) ? 1 : PM ? 4 : ldb, bstep8 = 8 * bstep1;
+  // register variant: slot J % 3 holds tile J's right-hand side pair and inverse
+  // fragments, loaded two tiles ahead (early tiles are shorter than a DRAM round trip)
+  double pb0[3], pb1[3], pw0[3], pw1[3];
+  auto ld_rhs = [&](int J, double& b0, double& b1) {
+    const int ca = 8 * J + 2 * t;
+    b0 = (rok && ca < n) ? brow[J * bstep8] : 0.0;
+    b1 = (rok && ca + 1 < n) ? brow[J * bstep8 + bstep1] : 0.0;
+  };
+  auto ld_inv = [&](int J, double& w0, double& w1) {
+    const double* w = R.W + (p * R.ntmax + J) * 64 + lane;
+    w0 = w[0];
+    w1 = w[32];
+  };
   double nb0 = (rok && 2 * t < n) ? brow[0] : 0.0;
   double nb1 = (rok && 2 * t + 1 < n) ? brow[bstep1] : 0.0;
+  if constexpr (DEEP) {
+    pb0[0] = nb0; pb1[0] = nb1; pw0[0] = wn0; pw1[0] = wn1;
+    pb0[1] = pb1[1] = pw0[1] = pw1[1] = 0.0;
+    if (nt > 1) { ld_rhs(1, pb0[1], pb1[1]); ld_inv(1, pw0[1], pw1[1]); }
+  }
 #pragma unroll
   for (int J = 0; J < (REG ? NT : 1 << 30); ++J) {
     if (J >= nt) break;
-    cp_async_wait_all();
+    if constexpr (REG) cp_async_wait_group1();
+    else cp_async_wait_all();
     __syncthreads();  // rows of tile J staged; every warp is done with tile J-1's buffer
-    if (J + 1 < nt) stage(J + 1);
-    const double* ab = ab_base + (J & 1) * abs;
+    if constexpr (REG) {
+      if (J + 2 < nt) stage(J + 2);
+      cp_async_commit();  // (an empty group keeps the count in step)
+    } else {
+      if (J + 1 < nt) stage(J + 1);
+    }
+    const double* ab = ab_base + (REG ? J % 3 : J & 1) * abs;
     const uint32_t abu = smem_u32(ab);
     const int ca = 8 * J + 2 * t, cb = ca + 1;
-    double acc0 = alpha * nb0, acc1 = alpha * nb1;
-    if (J + 1 < nt) {  // next tile's right-hand side, loaded under this tile's work
-      nb0 = (rok && ca + 8 < n) ? brow[(J + 1) * bstep8] : 0.0;
-      nb1 = (rok && cb + 8 < n) ? brow[(J + 1) * bstep8 + bstep1] : 0.0;
+    double acc0, acc1;
+    if constexpr (DEEP) {
+      acc0 = alpha * pb0[J % 3];
+      acc1 = alpha * pb1[J % 3];
+      if (J + 2 < nt) ld_rhs(J + 2, pb0[(J + 2) % 3], pb1[(J + 2) % 3]);
+    } else {
+      acc0 = alpha * nb0;
+      acc1 = alpha * nb1;
+      if (J + 1 < nt) {  // next tile's right-hand side, loaded under this tile's work
+        nb0 = (rok && ca + 8 < n) ? brow[(J + 1) * bstep8] : 0.0;
+        nb1 = (rok && cb + 8 < n) ? brow[(J + 1) * bstep8 + bstep1] : 0.0;
+      }
     }
     // ---- C -= X(:, 0:8J) A(J, 0:8J)^T ----
     double e0 = 0.0, e1 = 0.0;  // second accumulator pair: two independent DMMA chains
@@ -258,11 +300,15 @@ __global__ void __launch_bounds__(32 * kRltWarps, NT > 20 ? 3 : NT > 12 ? 4 : NT
       const int s0 = (lane & ~3) | (t >> 1), s1 = (lane & ~3) | (2 + (t >> 1));
       const double u00 = __shfl_sync(0xffffffffu, acc0, s0), u01 = __shfl_sync(0xffffffffu, acc1, s0);
       const double u10 = __shfl_sync(0xffffffffu, acc0, s1), u11 = __shfl_sync(0xffffffffu, acc1, s1);
-      const double w0 = wn0, w1 = wn1;
-      if (J + 1 < nt) {  // next tile's inverse fragments, loaded under this tile's solve
-        const double* w = R.W + (p * R.ntmax + J + 1) * 64 + lane;
-        wn0 = w[0];
-        wn1 = w[32];
+      double w0, w1;
+      if constexpr (DEEP) {
+        w0 = pw0[J % 3];
+        w1 = pw1[J % 3];
+        if (J + 2 < nt) ld_inv(J + 2, pw0[(J + 2) % 3], pw1[(J + 2) % 3]);
+      } else {
+        w0 = wn0;
+        w1 = wn1;
+        if (J + 1 < nt) ld_inv(J + 1, wn0, wn1);  // next tile's inverse fragments, under this tile's solve
       }
       acc0 = acc1 = 0.0;
       dmma(acc0, acc1, (t & 1) ? u01 : u00, w0);
@@ -328,7 +374,8 @@ cudaError_t trsm_rlt_launch(const TrsmLaunch& L, cudaStream_t s) {
   }();
   // (measured: no gain up to 8 tiles, 1.2x at 16, 1.6x at 32)
   const int ntr = !reg_ok || R.ntmax <= 8 || R.ntmax > 32 ? 0 : ((R.ntmax + 3) & ~3);  // a multiple of 4 tiles
-  const size_t smem = (size_t)((ntr ? 0 : kRltWarps) + 2) * R.ntmax * 64 * sizeof(double);  // [X slices +] 2 staged A rows
+  // register variant: 3 staged A row buffers; shared variant: the warps' X slices + 2 buffers
+  const size_t smem = (size_t)(ntr ? 3 : kRltWarps + 2) * R.ntmax * 64 * sizeof(double);
   {
     cudaError_t e = smem_attr((const void*)(L.pm ? trsm_rlt_kernel<1, 0> : trsm_rlt_kernel<0, 0>), 200 * 1024);
     if (e != cudaSuccess) return e;
