@@ -15,7 +15,8 @@ for src, dst in (("bench_full.json", "r02_bench.json"), ("bench_ref.json", "r02_
                  ("getrf192_launches.txt", "r02_getrf192_launches.txt"),
                  ("potrf256_launches.txt", "r02_potrf256_launches.txt"),
                  ("dgemm64_details.csv", "r02_dgemm64_ncu_details.csv"),
-                 ("eng128_details.csv", "r02_engine128_ncu_details.csv")):
+                 ("eng128_details.csv", "r02_engine128_ncu_details.csv"),
+                 ("cfg2_all_sizes.json", "r02_cfg2_all_sizes.json")):
     if os.path.exists(os.path.join(G, src)):
         shutil.copyfile(os.path.join(G, src), os.path.join(P, dst))
 
@@ -29,11 +30,12 @@ K = {
     "potrf128": ("potrf128", 8192, 8 * 128 * 129, 128 ** 3 // 3),
     "engine_nt_pm128": ("eng128", (2 ** 31) // (32 * 128 * 128), 32 * 128 * 128, 2 * 128 ** 3),
     "engine_nt_pm132": ("eng132", (2 ** 31) // (32 * 132 * 132), 32 * 132 * 132, 2 * 132 ** 3),
+    "trsm_rlt256": ("trsm256", 1024, 8 * (256 * 257 // 2 + 2 * 256 * 256), 256 ** 3),
 }
 out = {"_note": "ncu --set full --clock-control none, one launch each (tools/capture_r02c.sh), round 2 after the "
                 "engine work: gemm_cm_kernel<8> (cfg1 16384 x 64^3), getrf_sq_kernel (cfg4 n = 48, 96; 8192 problems), "
                 "gemm_cmsmall_kernel<2> (16384 x 16^3), potrf_cta_kernel (cfg3 n = 64, 128; 8192 problems), "
-                "gemm_tiles_kernel (cfg2 NT panel-major s = 128 full tiles / s = 132 ragged tiles); "
+                "gemm_tiles_kernel (cfg2 NT panel-major s = 128 full tiles / s = 132 ragged tiles), trsm_rlt_kernel (X L^T = B, n = m = 256, 1024 problems); "
                 "dram bytes are per launch"}
 for name, (cap, nprob, by, fl) in K.items():
     f = os.path.join(G, cap + "_summary.json")
