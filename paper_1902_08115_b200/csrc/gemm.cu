@@ -384,10 +384,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
   // lane's first pair: f * sf + h * sh (no per-element bounds or index math)
   const long long sfc = OUT_PM ? 32 : 8LL * P.o.ldc, shc = OUT_PM ? 8LL * P.o.ldc : 8;
   const long long sfd = OUT_PM ? 32 : 8LL * P.o.ldd, shd = OUT_PM ? 8LL * P.o.ldd : 8;
-  // a tile whose 64 x 64 elements are all written with 16-byte pairs
+  // a tile moved as 16-byte pairs from one base pointer: aligned storage, an even
+  // m (a pair is inside or outside as a whole) and no uplo diagonal through it.
+  // Full-tile launches (EDGE = 0) move every pair; ragged ones predicate each
+  // pair on its row and column — no per-element masks or index arithmetic.
   auto interior = [&](int tm, int tn) {
-    return P.o.vec && (tm + 1) * TM <= P.m && (tn + 1) * TN <= P.n &&
-           (P.uplo == 0 || (P.uplo == 1 ? tm > tn : tm < tn));
+    if (!(P.o.vec && (P.uplo == 0 || (P.uplo == 1 ? tm > tn : tm < tn)))) return false;
+    if (EDGE) return (P.m & 1) == 0;
+    return (tm + 1) * TM <= P.m && (tn + 1) * TN <= P.n;
   };
   // beta*C operands for this lane's 4x2 fragments, prefetched one item ahead
   // so their DRAM latency hides behind a whole item of tensor-core work.
@@ -397,12 +401,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
         P.o.c + (P.o.offs_c ? P.o.offs_c[p] : P.o.offs ? P.o.offs[p] : (long long)p * P.o.sc);
     const bool live = !(P.skip && P.skip[p]);
     if (live && interior(tm, tn)) {
-      const double* cp0 = cbase + out_off<OUT_PM>(P.o.ldc, tm * TM + ib + 2 * t, tn * TN + jb + g);
+      const int ir = tm * TM + ib + 2 * t, jr = tn * TN + jb + g;
+      const double* cp0 = cbase + out_off<OUT_PM>(P.o.ldc, ir, jr);
 #pragma unroll
       for (int f = 0; f < WF; ++f)
 #pragma unroll
         for (int h = 0; h < WH; ++h) {
-          const double2 v = *reinterpret_cast<const double2*>(cp0 + f * sfc + h * shc);
+          double2 v = make_double2(0.0, 0.0);
+          if (!EDGE || (ir + 8 * h < P.m && jr + 8 * f < P.n)) v = *reinterpret_cast<const double2*>(cp0 + f * sfc + h * shc);
           dst[f][h][0] = v.x;
           dst[f][h][1] = v.y;
         }
@@ -490,14 +496,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
 
     // Epilogue: d = alpha*acc + beta*c, masked to the problem and the uplo triangle.
     if (interior(tm, tn)) {
-      double* dp0 = dbase + out_off<OUT_PM>(P.o.ldd, i0 + ib + 2 * t, j0 + jb + g);
+      const int ir = i0 + ib + 2 * t, jr = j0 + jb + g;
+      double* dp0 = dbase + out_off<OUT_PM>(P.o.ldd, ir, jr);
 #pragma unroll
       for (int f = 0; f < WF; ++f)
 #pragma unroll
         for (int h = 0; h < WH; ++h) {
           const double r0 = use_c ? fma(P.alpha, acc[f][h][0], P.beta * cv[f][h][0]) : acc[f][h][0] * P.alpha;
           const double r1 = use_c ? fma(P.alpha, acc[f][h][1], P.beta * cv[f][h][1]) : acc[f][h][1] * P.alpha;
-          *reinterpret_cast<double2*>(dp0 + f * sfd + h * shd) = make_double2(r0, r1);
+          if (!EDGE || (ir + 8 * h < P.m && jr + 8 * f < P.n))
+            *reinterpret_cast<double2*>(dp0 + f * sfd + h * shd) = make_double2(r0, r1);
         }
       continue;
     }
