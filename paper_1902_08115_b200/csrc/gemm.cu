@@ -487,10 +487,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tiles_kernel(const __grid_co
       int ha = min(WH, max(0, (P.m - i0 - ib + 7) >> 3)), fa = min(WF, max(0, (P.n - j0 - jb + 7) >> 3));
       if (P.uplo && tm == tn && (P.uplo == 1 ? ib + 8 * WH - 1 < jb : jb + 8 * WF - 1 < ib)) fa = 0;
       if (ha == 0) fa = 0;
-      if (fa == WF && ha == WH) PB_KL(4, 2);
+      // (three live column fragments run as four: seven variants instead of nine —
+      // different warps run different variants at once and the kernel is sensitive
+      // to its code size; a single fragment, the thin edge tile, keeps its own)
+      if (fa > 2 && ha == WH) PB_KL(4, 2);
       else if (fa == 0) PB_KL(0, 0);
-      else if (ha == 2) { if (fa == 3) PB_KL(3, 2); else if (fa == 2) PB_KL(2, 2); else PB_KL(1, 2); }
-      else { if (fa == 4) PB_KL(4, 1); else if (fa == 3) PB_KL(3, 1); else if (fa == 2) PB_KL(2, 1); else PB_KL(1, 1); }
+      else if (ha == 2) { if (fa == 2) PB_KL(2, 2); else PB_KL(1, 2); }
+      else if (fa > 2) PB_KL(4, 1);
+      else if (fa == 2) PB_KL(2, 1);
+      else PB_KL(1, 1);
     }
 #undef PB_KL
 
