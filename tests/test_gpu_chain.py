@@ -187,3 +187,42 @@ def test_chain_host_plan_and_host_pointers(pb, cuda, layout):
     for other in runs[1:]:
         assert (other[2] == 0).all()
         assert same_bits(other[0], runs[0][0]) and same_bits(other[1], runs[0][1])
+
+
+def test_chain_cm_odd_orders_take_the_workspace_path(pb, orc, cuda):
+    """Column-major chain with odd orders: the offsets are odd, so the large orders cannot ride
+    the engine's offset tensor maps in place (16-byte alignment) and go through the gathered
+    strided workspace instead; same results, strict upper triangle of C untouched."""
+    import torch
+    rng = np.random.default_rng(77)
+    ns = np.array([5, 33, 161, 163, 201, 255, 170, 64, 7, 199], dtype=np.int64)
+    batch = len(ns)
+    offs = np.concatenate([[0], np.cumsum(ns ** 2)[:-1]])
+    total = int((ns ** 2).sum())
+    A = rng.uniform(-1, 1, total); B = rng.uniform(-1, 1, total)
+    C = rng.uniform(-1, 1, total)  # the strict upper part is noise that must survive
+    for p, n in enumerate(ns):
+        blk = C[offs[p]:offs[p] + n * n].reshape(n, n, order="F")
+        blk[np.tril_indices(n)] = 0.0
+        blk[np.arange(n), np.arange(n)] = n
+    C0 = C.copy()
+    dA, dB, dC = (torch.from_numpy(x.copy()).to(cuda) for x in (A, B, C))
+    dn = torch.from_numpy(ns.astype(np.int32)).to(cuda)
+    doff = torch.from_numpy(offs.astype(np.int64)).to(cuda)
+    info = torch.full((batch,), -9, dtype=torch.int32, device=cuda)
+    r = pb.chain_vbatched("C", dn, doff, dA, dC, dB, info, batch, int(ns.max()))
+    assert r.ok(), r
+    gC, gB, gi = dC.cpu().numpy(), dB.cpu().numpy(), info.cpu().numpy()
+    assert (gi == 0).all()
+    for p, n in enumerate(ns):
+        n = int(n); o = offs[p]
+        a, c, b = (np.asfortranarray(x[o:o + n * n].reshape(n, n, order="F").copy()) for x in (A, C0, B))
+        orc.dsyrk(b"l", b"n", n, n, 1.0, ptr(a), n, 1.0, ptr(c), n)
+        assert orc.dpotrf(b"l", n, ptr(c), n) == 0
+        assert orc.dtrsm(b"r", b"l", b"t", b"n", n, n, 1.0, ptr(c), n, ptr(b), n) == 0
+        gc = gC[o:o + n * n].reshape(n, n, order="F"); gb = gB[o:o + n * n].reshape(n, n, order="F")
+        lo = np.tril(np.ones((n, n), bool))
+        assert rel_frob(gc[lo], c[lo]) <= tol(n)
+        assert rel_frob(gb, b) <= tol(n) * 10
+        up = np.triu(np.ones((n, n), bool), 1)
+        assert np.array_equal(gc[up], C0[o:o + n * n].reshape(n, n, order="F")[up])
