@@ -41,8 +41,14 @@ constexpr int kRegWarps = 4;
 
 // CS != 0: compile-time column stride (packed column-major lower problems,
 // lda == n == N): every access is the row pointer plus an immediate offset.
+#ifndef PB_REG_LATE_FROM
+#define PB_REG_LATE_FROM 32
+#endif
+#ifndef PB_REG_BLOCKS32
+#define PB_REG_BLOCKS32 4
+#endif
 template <int N, int W, int PM, int CS, int RR>
-__global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_kernel(const __grid_constant__ PotrfRegArgs P) {
+__global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? PB_REG_BLOCKS32 : 4)) potrf_reg_kernel(const __grid_constant__ PotrfRegArgs P) {
   // RR rows per lane: lane i of a W-lane segment owns rows i, i + W, ... (N <= W * RR)
   static_assert(N <= W * RR && W <= 32 && 32 % W == 0, "segment shape");
   constexpr int SEGS = 32 / W;
@@ -77,21 +83,41 @@ __global__ void __launch_bounds__(32 * kRegWarps, (N >= 32 ? 3 : 4)) potrf_reg_k
 #pragma unroll
     for (int q = 0; q < RR; ++q) sts64(buf + 8u * (i + W * q), x[q][c]);
     __syncwarp();
+    // N >= 32: only the pivot now, the multipliers a(c2, c) are read pair by pair next to
+    // their use — holding the whole column would cost 64 registers and a resident CTA
+    constexpr bool LATE = N >= PB_REG_LATE_FROM;
     double col[N];
+    if constexpr (LATE) {
+      col[c] = lds64(buf + 8u * c);
+    } else {
 #pragma unroll
-    for (int c2 = c & ~1; c2 < N; c2 += 2) lds128(buf + 8u * c2, col[c2], col[c2 + 1]);
+      for (int c2 = c & ~1; c2 < N; c2 += 2) lds128(buf + 8u * c2, col[c2], col[c2 + 1]);
+    }
     const double piv = col[c];  // == x[.][c] on the row c
     bad |= (piv <= 0.0 ? 1u : 0u) << c;
     infp |= (piv == __longlong_as_double(0x7ff0000000000000LL) ? 1u : 0u) << c;
     double inv = rsqrt_nb(piv);
     // denormal / +inf pivots: CUDA's full rsqrt (within 1 ulp of the reference's 1 / sqrt(piv))
     if (__any_sync(0xffffffffu, rsqrt_special(piv))) inv = rsqrt_special(piv) ? rsqrt(piv) : inv;
+    if constexpr (LATE) {
+      static_assert(!LATE || RR == 1, "late multiplier loads are written for one row per lane");
+      x[0][c] *= inv;
+      const double t = x[0][c] * inv;
 #pragma unroll
-    for (int q = 0; q < RR; ++q) {
-      x[q][c] *= inv;
-      const double t = x[q][c] * inv;
+      for (int c2 = (c + 1) & ~1; c2 < N; c2 += 2) {
+        double u0, u1;
+        lds128(buf + 8u * c2, u0, u1);
+        if (c2 > c) x[0][c2] = fma(-t, u0, x[0][c2]);
+        x[0][c2 + 1] = fma(-t, u1, x[0][c2 + 1]);
+      }
+    } else {
 #pragma unroll
-      for (int c2 = c + 1; c2 < N; ++c2) x[q][c2] = fma(-t, col[c2], x[q][c2]);
+      for (int q = 0; q < RR; ++q) {
+        x[q][c] *= inv;
+        const double t = x[q][c] * inv;
+#pragma unroll
+        for (int c2 = c + 1; c2 < N; ++c2) x[q][c2] = fma(-t, col[c2], x[q][c2]);
+      }
     }
   }
   const unsigned nmask = n >= 32 ? 0xffffffffu : ((1u << n) - 1u);

@@ -2,6 +2,7 @@ import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, statistics
 import paper_1902_08115_b200 as pb
+if os.environ.get('PBGPU_LIB'): pb.library_path = os.path.abspath(os.environ['PBGPU_LIB'])  # A/B against another build
 dev = torch.device('cuda:0'); s = torch.cuda.current_stream()
 ns = [int(x) for x in sys.argv[1:]] or [16, 32, 64, 128, 256]
 for n in ns:
