@@ -405,7 +405,9 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
     mbar_wait(&sh_bar[0], 0);
   
   } else {
-    const bool pairs = !PM && !P.upper && (sld % 2 == 0) && ((reinterpret_cast<uintptr_t>(sa) & 15) == 0);
+    // 16-byte pairs of rows (2q, 2q + 1): contiguous in column-major storage with an even
+    // leading dimension, and always in panel-major storage (rows 4j .. 4j + 3 of a column)
+    const bool pairs = !P.upper && (PM || sld % 2 == 0) && ((reinterpret_cast<uintptr_t>(sa) & 15) == 0);
     for (int k = 0; k < TT; ++k) {
       double* pan = sm + cta_pbase(T, k);
       const int RS = cta_pstride(T, k), r0 = 8 * k, nr = min(n, 8 * TT) - r0;
@@ -415,8 +417,9 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
         for (int e = tid; e < tot; e += NTH) {
           const int c = e / np, q = e - c * np;
           if (r0 + c >= n) continue;
-          if (2 * q + 1 < nr) cp_async16(&pan[c * RS + 2 * q], src + c * sld + 2 * q);
-          else cp_async8(&pan[c * RS + 2 * q], src + c * sld + 2 * q, true);
+          const double* s2 = PM ? sa + cta_eoff<PM>(0, sld, r0 + 2 * q, r0 + c) : src + c * sld + 2 * q;
+          if (2 * q + 1 < nr) cp_async16(&pan[c * RS + 2 * q], s2);
+          else cp_async8(&pan[c * RS + 2 * q], s2, true);
         }
       } else {
         const int tot = 8 * nr;
@@ -584,6 +587,31 @@ __global__ void __launch_bounds__(32 * (NU + 1)) potrf_cta_kernel(const __grid_c
     }
     bulk_commit();
     bulk_wait_read0();
+  } else if (PM && !fail && ((reinterpret_cast<uintptr_t>(a) & 15) == 0)) {
+    // panel-major, no failure: rows (2q, 2q + 1) of a column are adjacent — 16-byte stores
+    // for the pairs wholly in the lower triangle, single elements across the diagonal
+    // (and the LowerZero zeros of the diagonal block's upper part when asked for)
+    for (int kb = 0; kb < TT; ++kb) {
+      const uint32_t pb = sbase + 8u * cta_pbase(T, kb);
+      const int RS = cta_pstride(T, kb), r0 = 8 * kb, rows = min(n, 8 * TT) - r0, np = (rows + 1) >> 1;
+      for (int e = tid; e < 8 * np; e += NTH) {
+        const int c = e / np, r = 2 * (e - c * np), row = r0 + r, col = r0 + c;
+        if (col >= n) continue;
+        double* dp = a + cta_eoff<PM>(0, lda, row, col);
+        if (r >= c && row + 1 < n) {
+          double v0, v1;
+          lds128(pb + 8u * (c * RS + r), v0, v1);
+          *reinterpret_cast<double2*>(dp) = make_double2(v0, v1);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (row + u >= n) continue;
+            if (r + u >= c) dp[u] = lds64(pb + 8u * (c * RS + r + u));
+            else if (zf) dp[u] = 0.0;
+          }
+        }
+      }
+    }
   } else {
     for (int kb = 0; kb * 8 < ncols; ++kb) {
       const uint32_t pb = sbase + 8u * cta_pbase(T, kb);
